@@ -1,0 +1,331 @@
+"""paper_2504_21440_b200 — B200-native (sm_100a) time-evolution engine for the
+QuantumToolbox.jl reference hot path (sesolve / mesolve / mcsolve, Liouvillian store,
+Dormand-Prince 5(4) integrator, Monte-Carlo trajectories, ensembles and sweeps).
+
+This module is a thin ctypes binding of the in-tree C-ABI library ``lib/libqsim_b200.so``
+(declared in ``include/qsg.h`` and ``include/qsg_model.h``). It exists for the test-suite,
+``bench.py`` and Python users; the compute path is CUDA only. There is no CPU fallback:
+importing works without a GPU, but every solver call raises ``QsgError`` when the library
+or a B200 device is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libqsim_b200.so")
+_lib = None
+
+P = C.c_void_p
+DP = C.POINTER(C.c_double)
+I32P = C.POINTER(C.c_int32)
+I64P = C.POINTER(C.c_int64)
+
+STATUS_NAMES = {
+    0: "OK", 1: "KindMismatch", 2: "DimsMismatch", 3: "InvalidSubsystem", 4: "InvalidDimension",
+    5: "InvalidIndex", 6: "TooLarge", 7: "IntegrationFailure", 8: "EnsembleFailure",
+    9: "SteadyStateFailure", 10: "DfdOverflow", 11: "InvalidGrid", 12: "InvalidScenario",
+    100: "CudaError", 101: "NcclError", 102: "OutOfMemory", 103: "Unsupported",
+}
+
+COEFF_CONST, COEFF_PARAM, COEFF_PARAM_COS, COEFF_PARAM_SIN = range(4)
+
+
+class QsgError(RuntimeError):
+    """Raised for every non-OK status; ``code`` is the qsg_status value."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{STATUS_NAMES.get(code, code)}] {msg}")
+        self.code = code
+
+
+class _Csr(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64),
+                ("rowptr", I32P), ("col", I32P), ("val", DP)]
+
+
+class _Coeff(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("i", C.c_int32), ("j", C.c_int32),
+                ("re", C.c_double), ("im", C.c_double)]
+
+
+class _Gen(C.Structure):
+    _fields_ = [("n_terms", C.c_int32), ("ops", C.POINTER(P)), ("coeffs", C.POINTER(_Coeff))]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("method", C.c_int32), ("abstol", C.c_double), ("reltol", C.c_double),
+                ("dt_fixed", C.c_double), ("store_states", C.c_int32), ("n_saveat", C.c_int64),
+                ("saveat", DP), ("max_steps", C.c_int64)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("rejected", C.c_int64), ("rhs_evals", C.c_int64)]
+
+
+class _Timing(C.Structure):
+    _fields_ = [("kernel_ms", C.c_double), ("total_ms", C.c_double), ("attempts", C.c_int64),
+                ("grid_ctas", C.c_int32), ("lanes", C.c_int32)]
+
+
+class _McOut(C.Structure):
+    _fields_ = [("per_traj_expect", DP), ("block_sum", DP), ("n_ok", I64P), ("failed", I32P),
+                ("fail_time", DP), ("traj_stats", I64P), ("jump_count", I32P),
+                ("jump_time", DP), ("jump_channel", I32P), ("jump_capacity", C.c_int64)]
+
+
+def build(verbose: bool = False) -> None:
+    """Compile lib/libqsim_b200.so (sm_100a) in-tree."""
+    subprocess.run(["make", "-C", _PKG] + ([] if verbose else ["-s"]), check=True)
+
+
+def lib():
+    """Load the C-ABI library; raises QsgError when it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise QsgError(100, f"{LIB_PATH} is missing: run paper_2504_21440_b200.build()")
+        L = C.CDLL(LIB_PATH)
+        L.qsg_last_error.restype = C.c_char_p
+        L.qsg_ctx_create.argtypes = [C.c_int, C.POINTER(P)]
+        L.qsg_ctx_destroy.argtypes = [P]
+        L.qsg_device_info.argtypes = [P, C.POINTER(C.c_int), I64P, C.c_char_p, C.c_int]
+        L.qsg_op_create.argtypes = [P, C.POINTER(_Csr), C.POINTER(P)]
+        L.qsg_op_destroy.argtypes = [P]
+        L.qsg_op_nnz.restype = C.c_int64
+        L.qsg_op_nnz.argtypes = [P]
+        L.qsg_generator_apply.argtypes = [P, C.POINTER(_Gen), DP, C.c_int32, C.c_double, DP, DP]
+        L.qsg_generator_apply_timed.argtypes = [P, C.POINTER(_Gen), DP, C.c_int32, C.c_double, P, P,
+                                                C.c_int32, DP]
+        for f in (L.qsg_mesolve, L.qsg_sesolve):
+            f.argtypes = [P, C.POINTER(_Gen), C.c_int64, P, DP, C.c_int64, C.c_int32, C.POINTER(_Csr),
+                          DP, C.c_int32, C.POINTER(_Opts), P, P, C.POINTER(_Stats), C.POINTER(_Timing)]
+        L.qsg_mcsolve.argtypes = [P, C.POINTER(_Gen), C.c_int32, C.POINTER(_Csr), C.c_int32,
+                                  C.POINTER(_Csr), C.c_int64, DP, DP, C.c_int64, DP, C.c_int32,
+                                  C.c_uint64, C.c_int64, C.c_int64, C.POINTER(_Opts),
+                                  C.POINTER(_McOut), C.POINTER(_Timing)]
+        L.qsg_ensemble_combine.argtypes = [C.c_int32, I64P, I64P, DP, C.c_int64, C.c_int64, DP]
+        L.qsg_mesolve_batch.argtypes = [P, C.POINTER(_Gen), C.c_int64, DP, DP, C.c_int64, C.c_int32,
+                                        C.POINTER(_Csr), C.c_int64, DP, C.c_int32, C.POINTER(_Opts),
+                                        DP, C.POINTER(_Stats), I32P, C.POINTER(_Timing)]
+        L.qsg_rng_draw.argtypes = [P, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, DP,
+                                   C.POINTER(C.c_uint64)]
+        _bind_model_api(L)
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise QsgError(rc, lib().qsg_last_error().decode())
+
+
+def _dp(a):
+    return None if a is None else a.ctypes.data_as(DP)
+
+
+def _ptr(a):
+    """Host numpy array or torch CUDA tensor -> void*."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    return C.c_void_p(a.ctypes.data)
+
+
+@dataclass
+class CsrMatrix:
+    """Host CSR (int32 indices, complex128 values) — the operator-store input format."""
+    rowptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+    n_rows: int
+    n_cols: int
+
+    @staticmethod
+    def from_arrays(rowptr, col, val, n_rows, n_cols=None):
+        return CsrMatrix(np.ascontiguousarray(rowptr, np.int32), np.ascontiguousarray(col, np.int32),
+                         np.ascontiguousarray(val, np.complex128), int(n_rows),
+                         int(n_rows if n_cols is None else n_cols))
+
+    @property
+    def nnz(self):
+        return len(self.val)
+
+    def _c(self) -> _Csr:
+        return _Csr(self.n_rows, self.n_cols, self.nnz, self.rowptr.ctypes.data_as(I32P),
+                    self.col.ctypes.data_as(I32P), self.val.ctypes.data_as(DP))
+
+
+class Context:
+    """One B200 device + stream (qsg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = P()
+        _check(lib().qsg_ctx_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+        sm = C.c_int(0)
+        l2 = C.c_int64(0)
+        name = C.create_string_buffer(256)
+        _check(lib().qsg_device_info(h, C.byref(sm), C.byref(l2), name, 256))
+        self.sm_count, self.l2_bytes, self.name = sm.value, l2.value, name.value.decode()
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            try:
+                _lib.qsg_ctx_destroy(self._h)
+            except TypeError:  # interpreter shutdown
+                pass
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def op(self, m: CsrMatrix) -> "Operator":
+        return Operator(self, m)
+
+
+class Operator:
+    """HBM-resident CSR operator (qsg_op)."""
+
+    def __init__(self, ctx: Context, m: CsrMatrix):
+        h = P()
+        c = m._c()
+        _check(lib().qsg_op_create(ctx._h, C.byref(c), C.byref(h)))
+        self._h, self.ctx, self.n, self.nnz = h, ctx, m.n_rows, m.nnz
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            try:
+                _lib.qsg_op_destroy(self._h)
+            except TypeError:  # interpreter shutdown
+                pass
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+class Generator:
+    """G(t) = A0 + sum_k c_k(params, t) A_k (SparseGenerator, evolve.cpp:53-69)."""
+
+    def __init__(self, ops, coeffs=None):
+        self.ops = list(ops)
+        self.coeffs = list(coeffs) if coeffs is not None else [(COEFF_CONST, 0, 0, 1.0, 0.0)] * len(self.ops)
+        self._arr = (P * len(self.ops))(*[o._h for o in self.ops])
+        self._carr = (_Coeff * len(self.ops))(*[_Coeff(*c) for c in self.coeffs])
+        self._g = _Gen(len(self.ops), C.cast(self._arr, C.POINTER(P)), C.cast(self._carr, C.POINTER(_Coeff)))
+
+    @property
+    def n(self):
+        return self.ops[0].n
+
+
+def _opts(abstol, reltol, max_steps, store_states, saveat):
+    sv = None if saveat is None else np.ascontiguousarray(saveat, np.float64)
+    o = _Opts(0, abstol, reltol, 1e-3, 1 if store_states else 0, 0 if sv is None else len(sv),
+              _dp(sv), max_steps)
+    return o, sv
+
+
+def _csr_array(ops):
+    arr = (_Csr * max(1, len(ops)))(*[o._c() for o in ops])
+    return arr
+
+
+def _num_saves(n_t, n_e, store_states, saveat):
+    if saveat is not None:
+        return len(np.union1d([], saveat))
+    return n_t if (store_states or n_e == 0) else 0
+
+
+def _solve(fn, ctx, gen, d, y0, tlist, e_ops, params, abstol, reltol, max_steps, store_states,
+           saveat, n_state):
+    t = np.ascontiguousarray(tlist, np.float64)
+    prm = None if params is None else np.ascontiguousarray(params, np.float64)
+    o, sv = _opts(abstol, reltol, max_steps, store_states, saveat)
+    eops = _csr_array(e_ops)
+    ne = len(e_ops)
+    expect = np.zeros(max(1, ne) * len(t), np.complex128)
+    nsave = _num_saves(len(t), ne, store_states, saveat)
+    states = np.zeros(nsave * n_state, np.complex128) if nsave else None
+    st, tm = _Stats(), _Timing()
+    y0h = y0 if hasattr(y0, "data_ptr") else np.ascontiguousarray(y0, np.complex128)
+    rc = fn(ctx._h, C.byref(gen._g), d, _ptr(y0h), _dp(t), len(t), ne, eops, _dp(prm),
+            0 if prm is None else len(prm), C.byref(o), _ptr(expect), _ptr(states), C.byref(st),
+            C.byref(tm))
+    _check(rc)
+    ex = expect[: ne * len(t)].reshape(len(t), ne).T.copy()
+    return {
+        "expect": ex,
+        "stats": (st.steps, st.rejected, st.rhs_evals),
+        "states": None if states is None else states.reshape(nsave, n_state),
+        "kernel_ms": tm.kernel_ms,
+        "attempts": tm.attempts,
+        "grid_ctas": tm.grid_ctas,
+        "lanes": tm.lanes,
+    }
+
+
+def mesolve(ctx: Context, L: Generator, d: int, rho0, tlist, e_ops=(), params=None, abstol=1e-8,
+            reltol=1e-6, max_steps=10_000_000, store_states=False, saveat=None):
+    """qsg_mesolve: rho0 is the d x d column-stacked density matrix (length d*d)."""
+    return _solve(lib().qsg_mesolve, ctx, L, d, rho0, tlist, list(e_ops), params, abstol, reltol,
+                  max_steps, store_states, saveat, d * d)
+
+
+def sesolve(ctx: Context, G: Generator, d: int, psi0, tlist, e_ops=(), params=None, abstol=1e-8,
+            reltol=1e-6, max_steps=10_000_000, store_states=False, saveat=None):
+    """qsg_sesolve with generator G = -i H."""
+    return _solve(lib().qsg_sesolve, ctx, G, d, psi0, tlist, list(e_ops), params, abstol, reltol,
+                  max_steps, store_states, saveat, d)
+
+
+def generator_apply(ctx: Context, gen: Generator, y, t=0.0, params=None):
+    y = np.ascontiguousarray(y, np.complex128)
+    out = np.zeros_like(y)
+    prm = None if params is None else np.ascontiguousarray(params, np.float64)
+    _check(lib().qsg_generator_apply(ctx._h, C.byref(gen._g), _dp(prm), 0 if prm is None else len(prm),
+                                     t, _dp(y), _dp(out)))
+    return out
+
+
+def generator_apply_timed(ctx: Context, gen: Generator, y_dev, out_dev, reps=20, t=0.0, params=None):
+    """Mean device ms of `reps` back-to-back applies on device (torch) buffers."""
+    prm = None if params is None else np.ascontiguousarray(params, np.float64)
+    ms = C.c_double(0)
+    _check(lib().qsg_generator_apply_timed(ctx._h, C.byref(gen._g), _dp(prm),
+                                           0 if prm is None else len(prm), t,
+                                           C.c_void_p(y_dev.data_ptr()), C.c_void_p(out_dev.data_ptr()),
+                                           reps, C.byref(ms)))
+    return ms.value
+
+
+def rng_draw(ctx: Context, seed: int, stream: int, kind: int, n: int):
+    if kind == 0:
+        out = np.zeros(n, np.uint64)
+        _check(lib().qsg_rng_draw(ctx._h, seed, stream, 0, n, None,
+                                  out.ctypes.data_as(C.POINTER(C.c_uint64))))
+    else:
+        out = np.zeros(n, np.float64)
+        _check(lib().qsg_rng_draw(ctx._h, seed, stream, kind, n, _dp(out), None))
+    return out
+
+
+def _bind_model_api(L):
+    """qsg_model_* entry points (include/qsg_model.h), if present in this build."""
+    if not hasattr(L, "qsg_model_create"):
+        return
+    L.qsg_model_create.argtypes = [C.c_char_p, DP, C.c_int32, C.POINTER(P)]
+    L.qsg_model_destroy.argtypes = [P]
+    L.qsg_model_info.argtypes = [P, I64P]
+    L.qsg_model_export.restype = C.c_int64
+    L.qsg_model_export.argtypes = [P, C.c_int32, C.c_int32, I64P, I32P, I32P, DP]
+    L.qsg_model_psi0.argtypes = [P, DP]
+    L.qsg_model_default_params.argtypes = [P, DP]

@@ -1,0 +1,213 @@
+// Shared device-side building blocks of the sm_100a time-evolution engines.
+//
+// Layout in HBM:
+//   operator store: CSR, int32 rowptr/col, complex128 values as double2 (16 B, 128-bit loads),
+//                   read with ld.global.nc.L1::no_allocate (streamed, never re-read in a pass);
+//   state vectors:  complex128 double2 arrays, one per DP5 register (y, y_old, k1..k7, two
+//                   stage-input buffers); every pass touches them coalesced, 32 rows per warp.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qsg {
+
+constexpr int kMaxTerms = 8;
+
+// Operator store: SELL-32 ("sliced ELLPACK", slice height 32 = one warp). Slice s holds rows
+// [32s, 32s+32); its entries are stored column-major inside the slice, so entry k of the 32 rows
+// is 32 consecutive (col, val) pairs — one fully coalesced 512 B value load per warp. Each row
+// keeps its true length; loads past it are predicated off, so padding costs no HBM bytes.
+struct DevSell {
+  const long long* slice_off;  // n_slices + 1, in units of 32-entry columns
+  const int* rowlen;           // n_slices * 32 (0 for rows past n)
+  const int* col;              // 32 * slice_off[n_slices]
+  const double2* val;
+  int n_rows;
+  int n_cols;
+  long long nnz;
+};
+
+struct DevCoeff {
+  int kind;  // qsg_coeff_kind
+  int i, j;
+  double re, im;
+};
+
+struct DevGen {
+  int n_terms;
+  DevSell A[kMaxTerms];
+  DevCoeff c[kMaxTerms];
+};
+
+// Dormand-Prince 5(4) tableau, error and dense-output weights, PI controller constants
+// (integrator.hpp:28-50). Values are the same double-precision literals.
+namespace dp {
+constexpr double c2 = 1.0 / 5.0, c3 = 3.0 / 10.0, c4 = 4.0 / 5.0, c5 = 8.0 / 9.0;
+constexpr double a21 = 1.0 / 5.0;
+constexpr double a31 = 3.0 / 40.0, a32 = 9.0 / 40.0;
+constexpr double a41 = 44.0 / 45.0, a42 = -56.0 / 15.0, a43 = 32.0 / 9.0;
+constexpr double a51 = 19372.0 / 6561.0, a52 = -25360.0 / 2187.0, a53 = 64448.0 / 6561.0,
+                 a54 = -212.0 / 729.0;
+constexpr double a61 = 9017.0 / 3168.0, a62 = -355.0 / 33.0, a63 = 46732.0 / 5247.0,
+                 a64 = 49.0 / 176.0, a65 = -5103.0 / 18656.0;
+constexpr double a71 = 35.0 / 384.0, a73 = 500.0 / 1113.0, a74 = 125.0 / 192.0,
+                 a75 = -2187.0 / 6784.0, a76 = 11.0 / 84.0;
+constexpr double e1 = 71.0 / 57600.0, e3 = -71.0 / 16695.0, e4 = 71.0 / 1920.0,
+                 e5 = -17253.0 / 339200.0, e6 = 22.0 / 525.0, e7 = -1.0 / 40.0;
+constexpr double d1 = -12715105075.0 / 11282082432.0, d3 = 87487479700.0 / 32700410799.0,
+                 d4 = -10690763975.0 / 1880347072.0, d5 = 701980252875.0 / 199316789632.0,
+                 d6 = -1453857185.0 / 822651844.0, d7 = 69997945.0 / 29380423.0;
+constexpr double beta = 0.04, expo1 = 0.2 - beta * 0.75, safe = 0.9;
+constexpr double facc1 = 5.0, facc2 = 0.1;
+}  // namespace dp
+
+// failure codes written by the device (mapped to reference messages on the host)
+enum DevStatus : int {
+  kRunning = 0,
+  kDone = 1,
+  kFailUnderflow = 2,   // integrator.hpp:84-86
+  kFailRejected = 3,    // integrator.hpp:87-89
+  kFailMaxSteps = 4,    // evolve.cpp:157-159, trajectories.cpp:147-149
+  kFailPastEnd = 5,     // integrator.hpp:83
+  kFailJumpWeights = 6, // trajectories.cpp:187-188
+  kFailJumpCapacity = 7 // device jump record buffer full (host re-runs with more room)
+};
+
+// ---- complex helpers (component order identical to std::complex / Eigen) ----------------
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+// acc += v * x with the product fused into two FMA chains.
+__device__ __forceinline__ void cfma(double2 v, double2 x, double2& acc) {
+  acc.x = fma(v.x, x.x, acc.x);
+  acc.x = fma(-v.y, x.y, acc.x);
+  acc.y = fma(v.x, x.y, acc.y);
+  acc.y = fma(v.y, x.x, acc.y);
+}
+__device__ __forceinline__ double cabs_(double2 a) { return hypot(a.x, a.y); }  // std::abs(complex)
+__device__ __forceinline__ double cnorm(double2 a) { return a.x * a.x + a.y * a.y; }
+
+__device__ __forceinline__ double2 coeff_eval(const DevCoeff& c, const double* params, double t) {
+  switch (c.kind) {
+    case 1: return make_double2(params[c.i], 0.0);
+    case 2: return make_double2(params[c.i] * cos(params[c.j] * t), 0.0);
+    case 3: return make_double2(params[c.i] * sin(params[c.j] * t), 0.0);
+    default: return make_double2(c.re, c.im);
+  }
+}
+
+// ---- streamed operator loads ----------------------------------------------------------------
+__device__ __forceinline__ int ld_stream(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// One row of a SELL-32 operator times a gathered vector (lane-per-row). XF maps col -> x[col].
+// Entries are consumed in ascending column order, as Eigen's CSC product accumulates a row.
+template <class XF>
+__device__ __forceinline__ double2 sell_row(const DevSell& A, int slice, int lane, XF&& xf) {
+  const int len = __ldg(A.rowlen + slice * 32 + lane);
+  const long long base = __ldg(A.slice_off + slice) * 32 + lane;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int j = 0; j < len; j += 8) {
+    int c[8];
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (j + u < len) {
+        c[u] = ld_stream(A.col + base + 32LL * (j + u));
+        v[u] = ld_stream(A.val + base + 32LL * (j + u));
+      } else {
+        c[u] = 0;
+        v[u] = make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j + u < len) cfma(v[u], xf(c[u]), acc);
+  }
+  return acc;
+}
+
+// Row `slice*32 + lane` of G(t) x with the reference term order: out = A0 x; out += c_k (A_k x)
+// (evolve.cpp:63-69). Rows past n return 0.
+template <class XF>
+__device__ __forceinline__ double2 gen_row(const DevGen& g, const double* params, int slice, double t,
+                                           XF&& xf) {
+  const int lane = threadIdx.x & 31;
+  double2 s = sell_row(g.A[0], slice, lane, xf);
+  for (int k = 1; k < g.n_terms; ++k) {
+    const double2 sk = sell_row(g.A[k], slice, lane, xf);
+    s = cadd(s, cmul(coeff_eval(g.c[k], params, t), sk));
+  }
+  return s;
+}
+
+// ---- block reduction (deterministic order) ----------------------------------------------------
+// Returns the block total on every thread. smem needs blockDim/32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (warp == 0) {
+    r = lane < nw ? smem[lane] : 0.0;
+    r = warp_sum(r);
+    if (lane == 0) smem[0] = r;
+  }
+  __syncthreads();
+  r = smem[0];
+  return r;
+}
+
+// ---- grid barrier for a cooperative launch ------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// bar[0] = arrival count, bar[1] = generation. All CTAs of the grid participate.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, int G) {
+  __syncthreads();
+  if (G > 1 && threadIdx.x == 0) {
+    const unsigned gen = ld_acquire_gpu(bar + 1);
+    __threadfence();
+    const unsigned arrived = atomicAdd(bar, 1u);
+    if (arrived == static_cast<unsigned>(G - 1)) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      st_release_gpu(bar + 1, gen + 1);
+    } else {
+      while (ld_acquire_gpu(bar + 1) == gen) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+}  // namespace qsg

@@ -1,0 +1,57 @@
+// Host <-> device contract of the persistent grid DP5 engine (grid_engine.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "engine.cuh"
+
+namespace qsg {
+
+constexpr int kMaxPending = 32;
+constexpr int kObsSlots = 128;  // doubles per observation slot bank (2 banks)
+enum : int { kSlotErr = 0, kSlotD0 = 1, kSlotD1 = 2, kSlotD2 = 3, kSlotObs0 = 4 };
+constexpr int kNumSlots = kSlotObs0 + 2 * kObsSlots;
+
+struct GridCtl {
+  double t, h, fail_t;
+  long long steps, rejected, rhs_evals, attempts;
+  int status;
+  int final_buf;
+};
+
+struct GridProblem {
+  int n;     // vector length (d*d for mesolve, d for sesolve)
+  int d;     // Hilbert dimension
+  DevGen gen;
+  const double* params;
+  double2* buf[11];
+  double atol, rtol;
+  long long max_steps;
+  double t0, tf, eps_t;
+  int n_ev;
+  const double* ev_t;
+  const int* ev_grid;
+  const int* ev_save;
+  int n_e;
+  // mesolve observation: e_op entries in CSC order, concatenated (evolve.cpp:288-295)
+  const int* eo_off;
+  const int* eo_i;
+  const int* eo_j;
+  const double2* eo_v;
+  // sesolve observation: e_ops as CSR, rowptr blocks of n+1 per op, col/val at se_off[e]
+  const int* se_rowptr;
+  const int* se_col;
+  const double2* se_val;
+  const long long* se_off;
+  double2* expect;  // n_e x n_grid, column-major
+  double2* states;  // n_save x n
+  GridCtl* ctl;
+  double* red;       // kNumSlots x G partials
+  unsigned* bar;     // grid barrier {count, generation}
+};
+
+int grid_threads();
+int grid_max_blocks_per_sm(int mode);
+cudaError_t launch_grid_dp5(const GridProblem& P, int mode, int grid, cudaStream_t s);
+
+}  // namespace qsg

@@ -1,0 +1,628 @@
+// C-ABI implementation: context, HBM operator store, generator apply, deterministic solvers.
+// Reference seams replaced are cited per entry point in include/qsg.h.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "grid_engine.h"
+#include "qsg_internal.h"
+
+namespace qsg {
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+qsg_status cuda_fail(cudaError_t e, const char* where) {
+  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? QSG_OUT_OF_MEMORY : QSG_CUDA_ERROR;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+cudaError_t upload(DevBuf& b, const void* src, size_t bytes, cudaStream_t s) {
+  cudaError_t e = b.alloc(bytes, s);
+  if (e != cudaSuccess || bytes == 0) return e;
+  return cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyDefault, s);
+}
+
+DevGen make_devgen(const qsg_generator* g) {
+  DevGen d{};
+  d.n_terms = g->n_terms;
+  for (int k = 0; k < g->n_terms; ++k) {
+    const qsg_op* op = g->ops[k];
+    d.A[k] = DevSell{op->slice_off, op->rowlen, op->col, op->val, static_cast<int>(op->n_rows),
+                     static_cast<int>(op->n_cols), op->nnz};
+    if (k > 0 && g->coeffs) {
+      const qsg_coeff& c = g->coeffs[k];
+      d.c[k] = DevCoeff{c.kind, c.i, c.j, c.re, c.im};
+    } else {
+      d.c[k] = DevCoeff{0, 0, 0, 1.0, 0.0};
+    }
+  }
+  return d;
+}
+
+qsg_status check_generator(const qsg_generator* g, long long n) {
+  if (!g || g->n_terms < 1 || g->n_terms > kMaxTerms || !g->ops) {
+    set_error("InvalidGrid: generator needs 1..8 terms");
+    return QSG_INVALID_GRID;
+  }
+  for (int k = 0; k < g->n_terms; ++k) {
+    const qsg_op* op = g->ops[k];
+    if (!op || op->n_rows != n || op->n_cols != n) {
+      set_error("DimsMismatch: generator term shape does not match the state");
+      return QSG_DIMS_MISMATCH;
+    }
+    if (k > 0 && g->coeffs && (g->coeffs[k].kind < 0 || g->coeffs[k].kind > 3)) {
+      set_error("InvalidGrid: unknown coefficient kind");
+      return QSG_INVALID_GRID;
+    }
+  }
+  return QSG_OK;
+}
+
+qsg_status check_tlist(const double* tlist, long long n_t) {  // evolve.cpp:71-75
+  if (n_t < 2) {
+    set_error("InvalidGrid: tlist needs at least two points");
+    return QSG_INVALID_GRID;
+  }
+  for (long long i = 1; i < n_t; ++i)
+    if (!(tlist[i] > tlist[i - 1])) {
+      set_error("InvalidGrid: tlist must increase strictly");
+      return QSG_INVALID_GRID;
+    }
+  return QSG_OK;
+}
+
+qsg_status build_events(const double* tlist, long long n_t, const qsg_solve_opts* o,
+                        bool keep_states, Events& ev) {
+  // evolve.cpp:89-118 with the saveat defaulting of :265-272
+  struct E {
+    double t;
+    int grid;
+    bool save;
+  };
+  std::vector<E> v;
+  for (long long i = 0; i < n_t; ++i) v.push_back({tlist[i], static_cast<int>(i), false});
+  std::vector<double> sv;
+  if (o && o->n_saveat > 0) sv.assign(o->saveat, o->saveat + o->n_saveat);
+  else if (keep_states) sv.assign(tlist, tlist + n_t);
+  if (!sv.empty()) {
+    if (!std::is_sorted(sv.begin(), sv.end())) {
+      set_error("InvalidGrid: saveat must be sorted");
+      return QSG_INVALID_GRID;
+    }
+    for (double t : sv) {
+      if (!(t >= tlist[0] && t <= tlist[n_t - 1])) {
+        set_error("InvalidGrid: saveat times must lie within [t0, tf]");
+        return QSG_INVALID_GRID;
+      }
+      v.push_back({t, -1, true});
+    }
+    std::stable_sort(v.begin(), v.end(), [](const E& a, const E& b) { return a.t < b.t; });
+    std::vector<E> merged;
+    for (const auto& e : v) {
+      if (!merged.empty() && merged.back().t == e.t) {
+        if (e.grid >= 0) merged.back().grid = e.grid;
+        merged.back().save |= e.save;
+      } else {
+        merged.push_back(e);
+      }
+    }
+    v.swap(merged);
+  }
+  ev = Events{};
+  for (const auto& e : v) {
+    ev.t.push_back(e.t);
+    ev.grid.push_back(e.grid);
+    ev.save.push_back(e.save ? ev.n_save++ : -1);
+  }
+  return QSG_OK;
+}
+
+static std::string fmt_t(double t) { return std::to_string(t); }  // std::to_string as reference
+
+qsg_status status_from_device(int st, double t) {
+  switch (st) {
+    case kDone: return QSG_OK;
+    case kFailUnderflow: set_error("IntegrationFailure: step size underflow at t = " + fmt_t(t)); break;
+    case kFailRejected: set_error("IntegrationFailure: step repeatedly rejected at t = " + fmt_t(t)); break;
+    case kFailMaxSteps: set_error("IntegrationFailure: max step count exceeded at t = " + fmt_t(t)); break;
+    case kFailPastEnd: set_error("IntegrationFailure: step called past t_end"); break;
+    case kFailJumpWeights: set_error("IntegrationFailure: vanishing jump weights at the crossing time"); break;
+    default: set_error("IntegrationFailure: solver did not finish"); break;
+  }
+  return QSG_INTEGRATION_FAILURE;
+}
+
+// ---- standalone generator apply (SparseGenerator::apply, evolve.cpp:63-69) ------------------
+__global__ void __launch_bounds__(256) gen_apply_kernel(DevGen g, const double* params, int n, double t,
+                                                        const double2* __restrict__ y,
+                                                        double2* __restrict__ out) {
+  const int W = blockDim.x >> 5;
+  const int nsl = (n + 31) >> 5;
+  for (int sl = blockIdx.x * W + (threadIdx.x >> 5); sl < nsl; sl += gridDim.x * W) {
+    const int row = (sl << 5) + (threadIdx.x & 31);
+    double2 k = gen_row(g, params, sl, t, [&](int c) { return y[c]; });
+    if (row < n) out[row] = k;
+  }
+}
+
+static cudaError_t launch_apply(const DevGen& dg, const double* params, int n, double t,
+                                const double2* y, double2* out, int sms, cudaStream_t s) {
+  const int threads = 256;
+  const int nsl = (n + 31) / 32;
+  const int grid = std::max(1, std::min((nsl + 7) / 8, sms * 8));
+  gen_apply_kernel<<<grid, threads, 0, s>>>(dg, params, n, t, y, out);
+  return cudaGetLastError();
+}
+
+// ---- CSR -> SELL-32 conversion on device -----------------------------------------------------
+__global__ void sell_widths_kernel(const int* rowptr, int n, int* rowlen, long long* width) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nsl = (n + 31) >> 5;
+  if (r >= nsl * 32) return;
+  const int len = r < n ? rowptr[r + 1] - rowptr[r] : 0;
+  rowlen[r] = len;
+  int m = len;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) width[r >> 5] = m;
+}
+
+__global__ void sell_fill_kernel(const int* rowptr, const int* col, const double2* val, int n,
+                                 const long long* slice_off, int* scol, double2* sval) {
+  const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int b = rowptr[r], e = rowptr[r + 1];
+  const long long base = slice_off[r >> 5] * 32 + (r & 31);
+  for (int k = 0; k < e - b; ++k) {
+    scol[base + 32LL * k] = col[b + k];
+    sval[base + 32LL * k] = val[b + k];
+  }
+}
+
+// ---- RNG kernel (rng.cpp:14-47) ---------------------------------------------------------------
+__device__ __forceinline__ unsigned long long d_splitmix(unsigned long long& s) {
+  unsigned long long z = (s += 0x9E3779B97F4A7C15ULL);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__global__ void rng_kernel(unsigned long long seed, unsigned long long stream, int kind, int n,
+                           double* out_d, unsigned long long* out_u) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long z = seed ^ ((stream + 1) * 0x9E3779B97F4A7C15ULL), s[4];
+  for (int i = 0; i < 4; ++i) s[i] = d_splitmix(z);
+  if ((s[0] | s[1] | s[2] | s[3]) == 0) s[0] = 1;
+  auto next = [&]() {
+    const unsigned long long r = ((s[0] + s[3]) << 23 | (s[0] + s[3]) >> 41) + s[0];
+    const unsigned long long tt = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= tt;
+    s[3] = (s[3] << 45) | (s[3] >> 19);
+    return r;
+  };
+  for (int i = 0; i < n; ++i) {
+    if (kind == 0) {
+      out_u[i] = next();
+    } else {
+      double u = static_cast<double>(next() >> 11) * 0x1.0p-53;
+      if (kind == 2)
+        while (u == 0.0) u = static_cast<double>(next() >> 11) * 0x1.0p-53;
+      out_d[i] = u;
+    }
+  }
+}
+
+// ---- shared deterministic-solver driver ----------------------------------------------------------
+static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G, long long d,
+                                 const double* y0, const double* tlist, long long n_t, int n_e,
+                                 const qsg_csr* e_ops, const double* params, int n_params,
+                                 const qsg_solve_opts* opts, double* expect, double* states,
+                                 qsg_stats* stats, qsg_timing* timing) {
+  if (!ctx) {
+    set_error("InvalidGrid: null context");
+    return QSG_INVALID_GRID;
+  }
+  if (qsg_status s = check_tlist(tlist, n_t)) return s;
+  const long long n = mode == 0 ? d * d : d;
+  if (n <= 0 || n > 0x7fffffffLL) {
+    set_error("TooLarge: state length must fit int32 indexing");
+    return QSG_TOO_LARGE;
+  }
+  if (qsg_status s = check_generator(G, n)) return s;
+  if (opts && opts->method != 0) {
+    set_error("InvalidGrid: only the adaptive Dormand-Prince 5(4) method runs on the device");
+    return QSG_UNSUPPORTED;
+  }
+  const double atol = opts ? opts->abstol : 1e-8, rtol = opts ? opts->reltol : 1e-6;
+  if (!(atol > 0 && rtol > 0)) {  // integrator.hpp:55
+    set_error("InvalidGrid: tolerances must be positive");
+    return QSG_INVALID_GRID;
+  }
+  const bool keep = (opts && opts->store_states) || n_e == 0;
+  Events ev;
+  if (qsg_status s = build_events(tlist, n_t, opts, keep, ev)) return s;
+  for (int e = 0; e < n_e; ++e)
+    if (e_ops[e].n_rows != d || e_ops[e].n_cols != d) {
+      set_error("DimsMismatch: e_ops dims mismatch");
+      return QSG_DIMS_MISMATCH;
+    }
+  if (2 * n_e > kObsSlots) {
+    set_error("TooLarge: at most 64 e_ops per solve");
+    return QSG_TOO_LARGE;
+  }
+  cudaStream_t s = ctx->stream;
+  cudaError_t ce;
+  // ---- workspace: 11 state vectors
+  const size_t vbytes = static_cast<size_t>(n) * sizeof(double2);
+  DevBuf work;
+  if ((ce = work.alloc(11 * vbytes, s))) return cuda_fail(ce, "workspace");
+  GridProblem P{};
+  P.n = static_cast<int>(n);
+  P.d = static_cast<int>(d);
+  for (int i = 0; i < 11; ++i) P.buf[i] = reinterpret_cast<double2*>(work.as<char>() + i * vbytes);
+  if ((ce = cudaMemcpyAsync(P.buf[0], y0, vbytes, cudaMemcpyDefault, s))) return cuda_fail(ce, "y0 copy");
+  P.gen = make_devgen(G);
+  DevBuf dparams;
+  if (n_params > 0) {
+    if ((ce = upload(dparams, params, sizeof(double) * n_params, s))) return cuda_fail(ce, "params");
+    P.params = dparams.as<double>();
+  }
+  P.atol = atol;
+  P.rtol = rtol;
+  P.max_steps = opts ? opts->max_steps : 10000000LL;
+  P.t0 = tlist[0];
+  P.tf = tlist[n_t - 1];
+  P.eps_t = 1e-12 * std::max({1.0, std::fabs(P.tf), std::fabs(P.t0)});  // evolve.cpp:128
+  DevBuf dev_t, dev_g, dev_s;
+  P.n_ev = static_cast<int>(ev.t.size());
+  if ((ce = upload(dev_t, ev.t.data(), ev.t.size() * sizeof(double), s))) return cuda_fail(ce, "events");
+  if ((ce = upload(dev_g, ev.grid.data(), ev.grid.size() * sizeof(int), s))) return cuda_fail(ce, "events");
+  if ((ce = upload(dev_s, ev.save.data(), ev.save.size() * sizeof(int), s))) return cuda_fail(ce, "events");
+  P.ev_t = dev_t.as<double>();
+  P.ev_grid = dev_g.as<int>();
+  P.ev_save = dev_s.as<int>();
+  P.n_e = n_e;
+  // ---- observation operators
+  std::vector<int> eo_off(1, 0), eo_i, eo_j, se_rowptr;
+  std::vector<double> eo_v;
+  std::vector<long long> se_off;
+  std::vector<int> se_col;
+  for (int e = 0; e < n_e; ++e) {
+    const qsg_csr& A = e_ops[e];
+    if (mode == 0) {
+      for (long long r = 0; r < A.n_rows; ++r)
+        for (int p = A.rowptr[r]; p < A.rowptr[r + 1]; ++p) {
+          eo_i.push_back(static_cast<int>(r));
+          eo_j.push_back(A.col[p]);
+          eo_v.push_back(A.val[2 * p]);
+          eo_v.push_back(A.val[2 * p + 1]);
+        }
+      eo_off.push_back(static_cast<int>(eo_i.size()));
+    } else {
+      se_off.push_back(static_cast<long long>(se_col.size()));
+      se_rowptr.insert(se_rowptr.end(), A.rowptr, A.rowptr + A.n_rows + 1);
+      se_col.insert(se_col.end(), A.col, A.col + A.nnz);
+      eo_v.insert(eo_v.end(), A.val, A.val + 2 * A.nnz);
+    }
+  }
+  DevBuf d_eoff, d_ei, d_ej, d_ev, d_srp, d_scol, d_soff;
+  if (mode == 0) {
+    if ((ce = upload(d_eoff, eo_off.data(), eo_off.size() * sizeof(int), s)) ||
+        (ce = upload(d_ei, eo_i.data(), eo_i.size() * sizeof(int), s)) ||
+        (ce = upload(d_ej, eo_j.data(), eo_j.size() * sizeof(int), s)) ||
+        (ce = upload(d_ev, eo_v.data(), eo_v.size() * sizeof(double), s)))
+      return cuda_fail(ce, "e_ops");
+    P.eo_off = d_eoff.as<int>();
+    P.eo_i = d_ei.as<int>();
+    P.eo_j = d_ej.as<int>();
+    P.eo_v = d_ev.as<double2>();
+  } else {
+    if ((ce = upload(d_srp, se_rowptr.data(), se_rowptr.size() * sizeof(int), s)) ||
+        (ce = upload(d_scol, se_col.data(), se_col.size() * sizeof(int), s)) ||
+        (ce = upload(d_ev, eo_v.data(), eo_v.size() * sizeof(double), s)) ||
+        (ce = upload(d_soff, se_off.data(), se_off.size() * sizeof(long long), s)))
+      return cuda_fail(ce, "e_ops");
+    P.se_rowptr = d_srp.as<int>();
+    P.se_col = d_scol.as<int>();
+    P.se_val = d_ev.as<double2>();
+    P.se_off = d_soff.as<long long>();
+  }
+  // ---- outputs and control
+  DevBuf d_exp, d_states, d_ctl, d_red, d_bar;
+  if ((ce = d_exp.alloc(std::max<size_t>(1, static_cast<size_t>(n_e) * n_t) * sizeof(double2), s)))
+    return cuda_fail(ce, "expect");
+  cudaMemsetAsync(d_exp.p, 0, std::max<size_t>(1, static_cast<size_t>(n_e) * n_t) * sizeof(double2), s);
+  P.expect = d_exp.as<double2>();
+  const bool states_dev = states && is_device_ptr(states);
+  if (ev.n_save > 0) {
+    if (states_dev) {
+      P.states = reinterpret_cast<double2*>(states);
+    } else {
+      if ((ce = d_states.alloc(static_cast<size_t>(ev.n_save) * vbytes, s))) return cuda_fail(ce, "states");
+      P.states = d_states.as<double2>();
+    }
+  }
+  const int lanes = 1;
+  const int threads = grid_threads();
+  const int per_sm = grid_max_blocks_per_sm(mode);
+  if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "occupancy");
+  const int max_grid = per_sm * ctx->sm_count;
+  const long long nblk = (n + 31) / 32;
+  int grid = static_cast<int>(std::min<long long>(max_grid, std::max<long long>(1, (n + 2047) / 2048)));
+  if (const char* eg = std::getenv("QSG_GRID")) grid = std::max(1, std::min(max_grid, std::atoi(eg)));
+  grid = static_cast<int>(std::min<long long>(grid, nblk));
+  (void)threads;
+  if ((ce = d_ctl.alloc(sizeof(GridCtl), s)) || (ce = d_red.alloc(sizeof(double) * kNumSlots * grid, s)) ||
+      (ce = d_bar.alloc(2 * sizeof(unsigned), s)))
+    return cuda_fail(ce, "control");
+  cudaMemsetAsync(d_bar.p, 0, 2 * sizeof(unsigned), s);
+  cudaMemsetAsync(d_ctl.p, 0, sizeof(GridCtl), s);
+  P.ctl = d_ctl.as<GridCtl>();
+  P.red = d_red.as<double>();
+  P.bar = d_bar.as<unsigned>();
+  cudaEventRecord(ctx->ev[0], s);
+  if ((ce = launch_grid_dp5(P, mode, grid, s))) return cuda_fail(ce, "solver launch");
+  cudaEventRecord(ctx->ev[1], s);
+  GridCtl ctl{};
+  if ((ce = cudaMemcpyAsync(&ctl, d_ctl.p, sizeof(GridCtl), cudaMemcpyDeviceToHost, s)))
+    return cuda_fail(ce, "ctl copy");
+  if ((ce = cudaStreamSynchronize(s))) return cuda_fail(ce, "solver");
+  if (stats) *stats = qsg_stats{ctl.steps, ctl.rejected, ctl.rhs_evals};
+  if (timing) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+    timing->kernel_ms = ms;
+    timing->attempts = ctl.attempts;
+    timing->grid_ctas = grid;
+    timing->lanes = lanes;
+  }
+  if (qsg_status st = status_from_device(ctl.status, ctl.fail_t)) return st;
+  if (expect && n_e > 0)
+    if ((ce = cudaMemcpyAsync(expect, d_exp.p, static_cast<size_t>(n_e) * n_t * sizeof(double2), cudaMemcpyDefault, s)))
+      return cuda_fail(ce, "expect copy");
+  if (states && ev.n_save > 0 && !states_dev)
+    if ((ce = cudaMemcpyAsync(states, P.states, static_cast<size_t>(ev.n_save) * vbytes, cudaMemcpyDefault, s)))
+      return cuda_fail(ce, "states copy");
+  if ((ce = cudaStreamSynchronize(s))) return cuda_fail(ce, "copy back");
+  return QSG_OK;
+}
+
+}  // namespace qsg
+
+using namespace qsg;
+
+extern "C" {
+
+const char* qsg_last_error(void) { return g_last_error.c_str(); }
+
+qsg_status qsg_ctx_create(int device, qsg_ctx** out) {
+  if (!out) return QSG_INVALID_GRID;
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    set_error(std::string("no CUDA device available: ") + cudaGetErrorString(e));
+    cudaGetLastError();
+    return QSG_CUDA_ERROR;
+  }
+  if (device < 0 || device >= ndev) {
+    set_error("InvalidIndex: device index out of range");
+    return QSG_INVALID_INDEX;
+  }
+  if ((e = cudaSetDevice(device))) return cuda_fail(e, "cudaSetDevice");
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, device))) return cuda_fail(e, "device properties");
+  if (prop.major < 10) {
+    set_error("this build targets sm_100a (B200); device is sm_" + std::to_string(prop.major * 10 + prop.minor));
+    return QSG_CUDA_ERROR;
+  }
+  auto* c = new qsg_ctx;
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  c->l2_bytes = prop.l2CacheSize;
+  std::snprintf(c->name, sizeof(c->name), "%s", prop.name);
+  if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking))) {
+    delete c;
+    return cuda_fail(e, "stream");
+  }
+  for (auto& ev : c->ev) cudaEventCreate(&ev);
+  *out = c;
+  return QSG_OK;
+}
+
+void qsg_ctx_destroy(qsg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& ev : ctx->ev) cudaEventDestroy(ev);
+  if (ctx->work) cudaFree(ctx->work);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+qsg_status qsg_device_info(qsg_ctx* ctx, int* sm_count, int64_t* l2_bytes, char* name, int name_len) {
+  if (!ctx) return QSG_INVALID_GRID;
+  if (sm_count) *sm_count = ctx->sm_count;
+  if (l2_bytes) *l2_bytes = ctx->l2_bytes;
+  if (name && name_len > 0) std::snprintf(name, name_len, "%s", ctx->name);
+  return QSG_OK;
+}
+
+qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
+  if (!ctx || !a || !out) {
+    set_error("InvalidGrid: null argument");
+    return QSG_INVALID_GRID;
+  }
+  *out = nullptr;
+  if (a->n_rows <= 0 || a->n_rows > 0x7fffffffLL || a->nnz < 0 || a->nnz > 0x7fffffffLL) {
+    set_error("TooLarge: operator exceeds int32 indexing");
+    return QSG_TOO_LARGE;
+  }
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const long long n = a->n_rows, nsl = (n + 31) / 32;
+  cudaError_t e;
+  // stage the CSR in HBM
+  DevBuf d_rp, d_col, d_val, d_w;
+  if ((e = upload(d_rp, a->rowptr, sizeof(int) * (n + 1), s)) ||
+      (e = upload(d_col, a->col, sizeof(int) * a->nnz, s)) ||
+      (e = upload(d_val, a->val, sizeof(double2) * a->nnz, s)) ||
+      (e = d_w.alloc(sizeof(long long) * nsl, s)))
+    return cuda_fail(e, "operator staging");
+  auto* op = new qsg_op;
+  op->ctx = ctx;
+  op->n_rows = n;
+  op->n_cols = a->n_cols;
+  op->nnz = a->nnz;
+  op->n_slices = nsl;
+  if ((e = cudaMalloc(&op->rowlen, sizeof(int) * nsl * 32)) ||
+      (e = cudaMalloc(&op->slice_off, sizeof(long long) * (nsl + 1)))) {
+    qsg_op_destroy(op);
+    return cuda_fail(e, "operator store allocation");
+  }
+  sell_widths_kernel<<<static_cast<unsigned>((nsl * 32 + 255) / 256), 256, 0, s>>>(d_rp.as<int>(), static_cast<int>(n),
+                                                                            op->rowlen, d_w.as<long long>());
+  std::vector<long long> w(nsl), off(nsl + 1, 0);
+  if ((e = cudaMemcpyAsync(w.data(), d_w.p, sizeof(long long) * nsl, cudaMemcpyDeviceToHost, s)) ||
+      (e = cudaStreamSynchronize(s))) {
+    qsg_op_destroy(op);
+    return cuda_fail(e, "operator widths");
+  }
+  for (long long i = 0; i < nsl; ++i) {
+    off[i + 1] = off[i] + w[i];
+    op->max_rowlen = std::max<int>(op->max_rowlen, static_cast<int>(w[i]));
+  }
+  op->padded_cols = off[nsl];
+  const size_t pe = static_cast<size_t>(std::max<long long>(1, off[nsl] * 32));
+  if ((e = cudaMalloc(&op->col, sizeof(int) * pe)) || (e = cudaMalloc(&op->val, sizeof(double2) * pe))) {
+    qsg_op_destroy(op);
+    return cuda_fail(e, "operator store allocation");
+  }
+  cudaMemsetAsync(op->col, 0, sizeof(int) * pe, s);
+  cudaMemsetAsync(op->val, 0, sizeof(double2) * pe, s);
+  cudaMemcpyAsync(op->slice_off, off.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, s);
+  sell_fill_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+      d_rp.as<int>(), d_col.as<int>(), d_val.as<double2>(), static_cast<int>(n), op->slice_off, op->col, op->val);
+  if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(s))) {
+    qsg_op_destroy(op);
+    return cuda_fail(e, "operator store build");
+  }
+  *out = op;
+  return QSG_OK;
+}
+
+void qsg_op_destroy(qsg_op* op) {
+  if (!op) return;
+  cudaFree(op->slice_off);
+  cudaFree(op->rowlen);
+  cudaFree(op->col);
+  cudaFree(op->val);
+  delete op;
+}
+
+int64_t qsg_op_nnz(const qsg_op* op) { return op ? op->nnz : 0; }
+int64_t qsg_op_rows(const qsg_op* op) { return op ? op->n_rows : 0; }
+
+qsg_status qsg_generator_apply(qsg_ctx* ctx, const qsg_generator* g, const double* params,
+                               int32_t n_params, double t, const double* y, double* out) {
+  if (!ctx || !g || g->n_terms < 1) return QSG_INVALID_GRID;
+  const long long n = g->ops[0]->n_rows;
+  if (qsg_status st = check_generator(g, n)) return st;
+  cudaStream_t s = ctx->stream;
+  cudaError_t e;
+  DevBuf dy, dout, dp;
+  const size_t vb = static_cast<size_t>(n) * sizeof(double2);
+  if ((e = upload(dy, y, vb, s)) || (e = dout.alloc(vb, s))) return cuda_fail(e, "apply buffers");
+  if (n_params > 0 && (e = upload(dp, params, sizeof(double) * n_params, s))) return cuda_fail(e, "params");
+  if ((e = launch_apply(make_devgen(g), dp.as<double>(), static_cast<int>(n), t, dy.as<double2>(),
+                        dout.as<double2>(), ctx->sm_count, s)))
+    return cuda_fail(e, "apply launch");
+  if ((e = cudaMemcpyAsync(out, dout.p, vb, cudaMemcpyDefault, s)) || (e = cudaStreamSynchronize(s)))
+    return cuda_fail(e, "apply");
+  return QSG_OK;
+}
+
+qsg_status qsg_generator_apply_timed(qsg_ctx* ctx, const qsg_generator* g, const double* params,
+                                     int32_t n_params, double t, const double* y_dev, double* out_dev,
+                                     int32_t reps, double* mean_ms) {
+  if (!ctx || !g || g->n_terms < 1 || reps < 1) return QSG_INVALID_GRID;
+  const long long n = g->ops[0]->n_rows;
+  if (qsg_status st = check_generator(g, n)) return st;
+  if (!is_device_ptr(y_dev) || !is_device_ptr(out_dev)) {
+    set_error("InvalidGrid: timed apply needs device buffers");
+    return QSG_INVALID_GRID;
+  }
+  cudaStream_t s = ctx->stream;
+  cudaError_t e;
+  DevBuf dp;
+  if (n_params > 0 && (e = upload(dp, params, sizeof(double) * n_params, s))) return cuda_fail(e, "params");
+  DevGen dg = make_devgen(g);
+  cudaEventRecord(ctx->ev[0], s);
+  for (int r = 0; r < reps; ++r)
+    if ((e = launch_apply(dg, dp.as<double>(), static_cast<int>(n), t,
+                          reinterpret_cast<const double2*>(y_dev), reinterpret_cast<double2*>(out_dev),
+                          ctx->sm_count, s)))
+      return cuda_fail(e, "apply launch");
+  cudaEventRecord(ctx->ev[1], s);
+  if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "apply");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+  if (mean_ms) *mean_ms = ms / reps;
+  return QSG_OK;
+}
+
+qsg_status qsg_mesolve(qsg_ctx* ctx, const qsg_generator* L, int64_t d, const double* rho0,
+                       const double* tlist, int64_t n_t, int32_t n_e, const qsg_csr* e_ops,
+                       const double* params, int32_t n_params, const qsg_solve_opts* opts,
+                       double* expect, double* states, qsg_stats* stats, qsg_timing* timing) {
+  if (ctx) cudaSetDevice(ctx->device);
+  return run_grid_solve(ctx, 0, L, d, rho0, tlist, n_t, n_e, e_ops, params, n_params, opts, expect,
+                        states, stats, timing);
+}
+
+qsg_status qsg_sesolve(qsg_ctx* ctx, const qsg_generator* G, int64_t d, const double* psi0,
+                       const double* tlist, int64_t n_t, int32_t n_e, const qsg_csr* e_ops,
+                       const double* params, int32_t n_params, const qsg_solve_opts* opts,
+                       double* expect, double* states, qsg_stats* stats, qsg_timing* timing) {
+  if (ctx) cudaSetDevice(ctx->device);
+  return run_grid_solve(ctx, 1, G, d, psi0, tlist, n_t, n_e, e_ops, params, n_params, opts, expect,
+                        states, stats, timing);
+}
+
+qsg_status qsg_rng_draw(qsg_ctx* ctx, uint64_t seed, uint64_t stream, int32_t kind, int32_t n,
+                        double* out_d, uint64_t* out_u) {
+  if (!ctx || n < 0) return QSG_INVALID_GRID;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  DevBuf bd, bu;
+  cudaError_t e;
+  if ((e = bd.alloc(sizeof(double) * std::max(1, n), s)) || (e = bu.alloc(sizeof(uint64_t) * std::max(1, n), s)))
+    return cuda_fail(e, "rng buffers");
+  rng_kernel<<<1, 32, 0, s>>>(seed, stream, kind, n, bd.as<double>(), bu.as<unsigned long long>());
+  if ((e = cudaGetLastError())) return cuda_fail(e, "rng launch");
+  if (kind == 0 && out_u) e = cudaMemcpyAsync(out_u, bu.p, sizeof(uint64_t) * n, cudaMemcpyDefault, s);
+  if (kind != 0 && out_d) e = cudaMemcpyAsync(out_d, bd.p, sizeof(double) * n, cudaMemcpyDefault, s);
+  if (e || (e = cudaStreamSynchronize(s))) return cuda_fail(e, "rng");
+  return QSG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// Internal host-side structures shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/qsg.h"
+#include "engine.cuh"
+
+struct qsg_ctx {
+  int device = 0;
+  int sm_count = 0;
+  long long l2_bytes = 0;
+  char name[256] = {0};
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // cached solver workspace
+  void* work = nullptr;
+  size_t work_bytes = 0;
+};
+
+// HBM operator store: SELL-32 layout (engine.cuh DevSell) built on device from the CSR input.
+struct qsg_op {
+  qsg_ctx* ctx = nullptr;
+  long long n_rows = 0, n_cols = 0, nnz = 0;
+  long long n_slices = 0, padded_cols = 0;  // padded_cols = slice_off[n_slices]
+  long long* slice_off = nullptr;
+  int* rowlen = nullptr;
+  int* col = nullptr;
+  double2* val = nullptr;
+  int max_rowlen = 0;
+};
+
+namespace qsg {
+
+void set_error(const std::string& msg);
+qsg_status cuda_fail(cudaError_t e, const char* where);
+bool is_device_ptr(const void* p);
+
+// RAII device buffer on the context stream (stream-ordered allocator).
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  cudaError_t alloc(size_t bytes, cudaStream_t st) {
+    s = st;
+    return cudaMallocAsync(&p, bytes ? bytes : 16, st);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Upload host-or-device array into a fresh device buffer.
+cudaError_t upload(DevBuf& b, const void* src, size_t bytes, cudaStream_t s);
+
+DevGen make_devgen(const qsg_generator* g);
+qsg_status check_generator(const qsg_generator* g, long long n);
+qsg_status check_tlist(const double* tlist, long long n_t);
+
+// evolve.cpp:89-118 build_events: tlist points (+ merged saveat) -> (t, grid index, save slot)
+struct Events {
+  std::vector<double> t;
+  std::vector<int> grid;
+  std::vector<int> save;
+  int n_save = 0;
+};
+qsg_status build_events(const double* tlist, long long n_t, const qsg_solve_opts* o,
+                        bool keep_states, Events& ev);
+
+qsg_status status_from_device(int st, double t);
+
+}  // namespace qsg
