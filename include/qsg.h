@@ -8,7 +8,7 @@
  *   - sesolve / mesolve                             evolve.hpp:81-91, evolve.cpp:191-299
  *   - mcsolve / run_ensemble / ensemble_stddev      trajectories.hpp:49-95, trajectories.cpp:11-249
  * Each entry point below replaces one of those seams with plain pointers and sizes; the C++
- * host library (include/qsim/*.hpp) builds operators exactly as the reference does and calls
+ * host library (include/qsim/ headers) builds operators exactly as the reference does and calls
  * these functions, so a reference user keeps the same solver API.
  *
  * Conventions (Eigen-compatible, qobj.hpp:15-19):

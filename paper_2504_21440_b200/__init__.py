@@ -319,9 +319,7 @@ def rng_draw(ctx: Context, seed: int, stream: int, kind: int, n: int):
 
 
 def _bind_model_api(L):
-    """qsg_model_* entry points (include/qsg_model.h), if present in this build."""
-    if not hasattr(L, "qsg_model_create"):
-        return
+    """qsg_model_* entry points (include/qsg_model.h)."""
     L.qsg_model_create.argtypes = [C.c_char_p, DP, C.c_int32, C.POINTER(P)]
     L.qsg_model_destroy.argtypes = [P]
     L.qsg_model_info.argtypes = [P, I64P]
@@ -329,3 +327,102 @@ def _bind_model_api(L):
     L.qsg_model_export.argtypes = [P, C.c_int32, C.c_int32, I64P, I32P, I32P, DP]
     L.qsg_model_psi0.argtypes = [P, DP]
     L.qsg_model_default_params.argtypes = [P, DP]
+    for f in (L.qsg_model_mesolve, L.qsg_model_sesolve):
+        f.argtypes = [P, C.c_int32, DP, C.c_int64, DP, C.c_int32, C.POINTER(_Opts), DP, I64P, DP]
+    L.qsg_model_mcsolve.argtypes = [P, C.c_int32, I32P, DP, C.c_int64, DP, C.c_int32, C.c_uint64, C.c_int32,
+                                    C.POINTER(_Opts), DP, DP, I64P, I32P, DP, I32P, C.c_int32, I32P, DP]
+
+
+# export selectors of qsg_model_export (include/qsg_model.h)
+SEL_H_CONST, SEL_H_TERM, SEL_C_OP, SEL_E_OP, SEL_L_CONST, SEL_L_TERM, SEL_MC_GEN, SEL_MC_TERM, SEL_SE_GEN = range(9)
+
+
+class Model:
+    """A BASELINE model assembled by the product's C++ host API (qsim::*, qsg_model.h)."""
+
+    def __init__(self, name: str, *params: float):
+        p = np.ascontiguousarray(params, np.float64)
+        h = P()
+        _check(lib().qsg_model_create(name.encode(), _dp(p), len(p), C.byref(h)))
+        self._h = h
+        self.name = name
+        info = np.zeros(6, np.int64)
+        lib().qsg_model_info(h, info.ctypes.data_as(I64P))
+        self.dim, self.n_terms, self.n_cops, self.n_eops, ket, npar = (int(x) for x in info)
+        self.psi0_is_ket = bool(ket)
+        self.default_params = np.zeros(npar)
+        if npar:
+            lib().qsg_model_default_params(h, _dp(self.default_params))
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            try:
+                _lib.qsg_model_destroy(self._h)
+            except TypeError:
+                pass
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def export(self, which: int, k: int = 0) -> CsrMatrix:
+        nrows = C.c_int64(0)
+        nnz = lib().qsg_model_export(self._h, which, k, C.byref(nrows), None, None, None)
+        if nnz < 0:
+            raise QsgError(11, lib().qsg_last_error().decode())
+        rp = np.zeros(nrows.value + 1, np.int32)
+        col = np.zeros(nnz, np.int32)
+        val = np.zeros(nnz, np.complex128)
+        lib().qsg_model_export(self._h, which, k, C.byref(nrows), rp.ctypes.data_as(I32P),
+                               col.ctypes.data_as(I32P), val.ctypes.data_as(DP))
+        return CsrMatrix(rp, col, val, nrows.value, nrows.value)
+
+    def psi0(self) -> np.ndarray:
+        out = np.zeros(self.dim if self.psi0_is_ket else self.dim * self.dim, np.complex128)
+        lib().qsg_model_psi0(self._h, out.ctypes.data_as(DP))
+        return out
+
+    def _solve(self, f, device, tlist, params, abstol, reltol, max_steps):
+        t = np.ascontiguousarray(tlist, np.float64)
+        prm = np.ascontiguousarray(self.default_params if params is None else params, np.float64)
+        o, _ = _opts(abstol, reltol, max_steps, False, None)
+        ex = np.zeros(self.n_eops * len(t), np.complex128)
+        st = np.zeros(3, np.int64)
+        ms = C.c_double(0)
+        _check(f(self._h, device, _dp(t), len(t), _dp(prm), len(prm), C.byref(o), _dp(ex),
+                 st.ctypes.data_as(I64P), C.byref(ms)))
+        return {"expect": ex.reshape(len(t), self.n_eops).T.copy(), "stats": tuple(int(x) for x in st),
+                "kernel_ms": ms.value}
+
+    def mesolve(self, tlist, params=None, device=0, abstol=1e-8, reltol=1e-6, max_steps=10_000_000):
+        """qsim::mesolve(H, psi0, tlist, c_ops, e_ops, params, options) on the device."""
+        return self._solve(lib().qsg_model_mesolve, device, tlist, params, abstol, reltol, max_steps)
+
+    def sesolve(self, tlist, params=None, device=0, abstol=1e-8, reltol=1e-6, max_steps=10_000_000):
+        return self._solve(lib().qsg_model_sesolve, device, tlist, params, abstol, reltol, max_steps)
+
+    def mcsolve(self, tlist, seed, ntraj, devices=(0,), params=None, abstol=1e-8, reltol=1e-6,
+                max_steps=10_000_000, jump_cap=256):
+        """qsim::mcsolve (trajectories sharded over `devices` in-process)."""
+        t = np.ascontiguousarray(tlist, np.float64)
+        prm = np.ascontiguousarray(self.default_params if params is None else params, np.float64)
+        o, _ = _opts(abstol, reltol, max_steps, False, None)
+        ne, nt = self.n_eops, len(t)
+        mean = np.zeros(ne * nt, np.complex128)
+        per = np.zeros(ntraj * ne * nt, np.complex128)
+        st = np.zeros(3, np.int64)
+        nj = np.zeros(ntraj, np.int32)
+        jt = np.zeros(ntraj * jump_cap)
+        jc = np.zeros(ntraj * jump_cap, np.int32)
+        nf = C.c_int32(0)
+        ms = C.c_double(0)
+        dv = np.ascontiguousarray(devices, np.int32)
+        _check(lib().qsg_model_mcsolve(self._h, len(dv), dv.ctypes.data_as(I32P), _dp(t), nt, _dp(prm), len(prm),
+                                       seed, ntraj, C.byref(o), _dp(mean), _dp(per), st.ctypes.data_as(I64P),
+                                       nj.ctypes.data_as(I32P), _dp(jt), jc.ctypes.data_as(I32P), jump_cap,
+                                       C.byref(nf), C.byref(ms)))
+        jumps = [list(zip(jt[i * jump_cap:i * jump_cap + min(nj[i], jump_cap)].tolist(),
+                          jc[i * jump_cap:i * jump_cap + min(nj[i], jump_cap)].tolist())) for i in range(ntraj)]
+        return {"mean": mean.reshape(nt, ne).T.copy(), "per_traj": per.reshape(ntraj, nt, ne).transpose(0, 2, 1).copy(),
+                "stats": tuple(int(x) for x in st), "njumps": nj, "jumps": jumps, "failed": nf.value,
+                "kernel_ms": ms.value}
