@@ -307,6 +307,86 @@ def generator_apply_timed(ctx: Context, gen: Generator, y_dev, out_dev, reps=20,
     return ms.value
 
 
+def mcsolve(ctx: Context, G: Generator, c_ops, e_ops, d: int, psi0, tlist, seed: int, traj_begin: int,
+            traj_end: int, params=None, abstol=1e-8, reltol=1e-6, max_steps=10_000_000, jump_cap=256,
+            per_traj=True):
+    """qsg_mcsolve: trajectories traj_begin..traj_end-1 of the ensemble (RngStream(seed, i))."""
+    t = np.ascontiguousarray(tlist, np.float64)
+    prm = None if params is None else np.ascontiguousarray(params, np.float64)
+    o, _ = _opts(abstol, reltol, max_steps, False, None)
+    ne, nt, nb = len(e_ops), len(t), traj_end - traj_begin
+    per = np.zeros(nb * ne * nt, np.complex128) if per_traj else None
+    bsum = np.zeros(max(1, ne * nt), np.complex128)
+    nok = C.c_int64(0)
+    failed = np.zeros(nb, np.int32)
+    ftime = np.zeros(nb)
+    tst = np.zeros(3 * nb, np.int64)
+    jcount = np.zeros(nb, np.int32)
+    jt = np.zeros(nb * jump_cap)
+    jc = np.zeros(nb * jump_cap, np.int32)
+    out = _McOut(_dp(per), _dp(bsum), C.pointer(nok), failed.ctypes.data_as(I32P), _dp(ftime),
+                 tst.ctypes.data_as(I64P), jcount.ctypes.data_as(I32P), _dp(jt), jc.ctypes.data_as(I32P),
+                 jump_cap)
+    tm = _Timing()
+    y0 = np.ascontiguousarray(psi0, np.complex128)
+    _check(lib().qsg_mcsolve(ctx._h, C.byref(G._g), len(c_ops), _csr_array(c_ops), ne, _csr_array(e_ops), d,
+                             _dp(y0), _dp(t), nt, _dp(prm), 0 if prm is None else len(prm), seed, traj_begin,
+                             traj_end, C.byref(o), C.byref(out), C.byref(tm)))
+    jumps = [list(zip(jt[i * jump_cap:i * jump_cap + min(jcount[i], jump_cap)].tolist(),
+                      jc[i * jump_cap:i * jump_cap + min(jcount[i], jump_cap)].tolist())) for i in range(nb)]
+    return {
+        "per_traj": None if per is None else per.reshape(nb, nt, ne).transpose(0, 2, 1).copy(),
+        "block_sum": bsum[: ne * nt].reshape(nt, ne).T.copy(),
+        "n_ok": nok.value,
+        "failed": failed,
+        "stats": tst.reshape(nb, 3),
+        "njumps": jcount,
+        "jumps": jumps,
+        "kernel_ms": tm.kernel_ms,
+        "attempts": tm.attempts,
+        "grid_ctas": tm.grid_ctas,
+    }
+
+
+def ensemble_combine(block_ranges, block_sums, n_ok_total):
+    """qsg_ensemble_combine: deterministic pairwise combine of per-block sums (mean)."""
+    b = np.ascontiguousarray([r[0] for r in block_ranges], np.int64)
+    e = np.ascontiguousarray([r[1] for r in block_ranges], np.int64)
+    sums = np.ascontiguousarray(np.stack([np.asarray(s).T.reshape(-1) for s in block_sums]), np.complex128)
+    nv = sums.shape[1]
+    mean = np.zeros(nv, np.complex128)
+    _check(lib().qsg_ensemble_combine(len(b), b.ctypes.data_as(I64P), e.ctypes.data_as(I64P), _dp(sums), nv,
+                                      n_ok_total, _dp(mean)))
+    shape = np.asarray(block_sums[0]).shape
+    return mean.reshape(shape[1], shape[0]).T.copy()
+
+
+def mesolve_batch(ctx: Context, L: Generator, d: int, rho0, tlist, e_ops, params, abstol=1e-8, reltol=1e-6,
+                  max_steps=10_000_000):
+    """qsg_mesolve_batch: one mesolve per row of `params` (n_points x n_params)."""
+    t = np.ascontiguousarray(tlist, np.float64)
+    prm = np.ascontiguousarray(params, np.float64)
+    npts, npar = prm.shape
+    o, _ = _opts(abstol, reltol, max_steps, False, None)
+    ne, nt = len(e_ops), len(t)
+    ex = np.zeros(npts * ne * nt, np.complex128)
+    st = (_Stats * npts)()
+    status = np.zeros(npts, np.int32)
+    tm = _Timing()
+    y0 = np.ascontiguousarray(rho0, np.complex128)
+    _check(lib().qsg_mesolve_batch(ctx._h, C.byref(L._g), d, _dp(y0), _dp(t), nt, ne, _csr_array(e_ops), npts,
+                                   _dp(prm), npar, C.byref(o), _dp(ex), st, status.ctypes.data_as(I32P),
+                                   C.byref(tm)))
+    return {
+        "expect": ex.reshape(npts, nt, ne).transpose(0, 2, 1).copy(),
+        "stats": np.array([(s.steps, s.rejected, s.rhs_evals) for s in st]),
+        "status": status,
+        "kernel_ms": tm.kernel_ms,
+        "attempts": tm.attempts,
+        "grid_ctas": tm.grid_ctas,
+    }
+
+
 def rng_draw(ctx: Context, seed: int, stream: int, kind: int, n: int):
     if kind == 0:
         out = np.zeros(n, np.uint64)

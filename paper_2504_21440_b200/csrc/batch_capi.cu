@@ -1,0 +1,319 @@
+// C-ABI of the batched engine: qsg_mcsolve (trajectories.cpp:106-249 + run_ensemble :26-92)
+// and qsg_mesolve_batch (one mesolve per parameter point, PAPER.md:647-652 pattern).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "batch_engine.h"
+#include "qsg_internal.h"
+
+using namespace qsg;
+
+namespace {
+
+struct TmpOps {
+  std::vector<qsg_op*> ops;
+  ~TmpOps() {
+    for (auto* o : ops) qsg_op_destroy(o);
+  }
+};
+
+qsg_status make_sell(qsg_ctx* ctx, const qsg_csr& a, TmpOps& keep, DevSell& out) {
+  qsg_op* op = nullptr;
+  if (qsg_status s = qsg_op_create(ctx, &a, &op)) return s;
+  keep.ops.push_back(op);
+  out = DevSell{op->slice_off, op->rowlen, op->col, op->val, static_cast<int>(op->n_rows),
+                static_cast<int>(op->n_cols), op->nnz};
+  return QSG_OK;
+}
+
+// pairwise_sum over [lo, hi) of the completed trajectories' matrices (trajectories.cpp:17-22)
+void pairwise(const std::vector<const double*>& m, size_t lo, size_t hi, size_t nv, double* out) {
+  if (hi - lo == 1) {
+    std::copy(m[lo], m[lo] + 2 * nv, out);
+    return;
+  }
+  const size_t mid = lo + (hi - lo) / 2;
+  std::vector<double> r(2 * nv);
+  pairwise(m, lo, mid, nv, out);
+  pairwise(m, mid, hi, nv, r.data());
+  for (size_t i = 0; i < 2 * nv; ++i) out[i] += r[i];
+}
+
+struct RunOut {
+  std::vector<double2> expect;
+  std::vector<int> status, jcount, jch;
+  std::vector<double> ftime, jtime;
+  std::vector<long long> stats;
+  double kernel_ms = 0;
+  long long attempts = 0;
+  int grid = 0;
+};
+
+// Runs systems [sys_begin, sys_begin + n_sys) through the batch kernel and downloads outputs.
+qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap, RunOut& o) {
+  cudaStream_t s = ctx->stream;
+  cudaError_t ce;
+  P.n_systems = n_sys;
+  P.jump_cap = jump_cap;
+  const int per_sm = batch_max_blocks_per_sm();
+  if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "batch occupancy");
+  long long want = (n_sys + batch_slots() - 1) / batch_slots();
+  int grid = static_cast<int>(std::min<long long>(static_cast<long long>(per_sm) * ctx->sm_count, want));
+  if (const char* eg = std::getenv("QSG_BATCH_GRID")) grid = std::max(1, std::min(grid, std::atoi(eg)));
+  o.grid = grid;
+  const size_t stride = batch_work_stride(P.n);
+  DevBuf work, q, ex, st, ft, stt, jc, jt, jch, att;
+  const size_t nvals = static_cast<size_t>(std::max(1, P.n_e)) * P.n_t;
+  if ((ce = work.alloc(stride * grid * sizeof(double2), s)) || (ce = q.alloc(8, s)) ||
+      (ce = ex.alloc(nvals * n_sys * sizeof(double2), s)) || (ce = st.alloc(sizeof(int) * n_sys, s)) ||
+      (ce = ft.alloc(sizeof(double) * n_sys, s)) || (ce = stt.alloc(sizeof(long long) * 3 * n_sys, s)) ||
+      (ce = jc.alloc(sizeof(int) * n_sys, s)) ||
+      (ce = jt.alloc(sizeof(double) * std::max<long long>(1, n_sys * jump_cap), s)) ||
+      (ce = jch.alloc(sizeof(int) * std::max<long long>(1, n_sys * jump_cap), s)) || (ce = att.alloc(8, s)))
+    return cuda_fail(ce, "batch workspace");
+  cudaMemsetAsync(q.p, 0, 8, s);
+  cudaMemsetAsync(att.p, 0, 8, s);
+  cudaMemsetAsync(ex.p, 0, nvals * n_sys * sizeof(double2), s);
+  cudaMemsetAsync(jc.p, 0, sizeof(int) * n_sys, s);
+  P.work = work.as<double2>();
+  P.work_stride = static_cast<long long>(stride);
+  P.queue = q.as<unsigned long long>();
+  P.expect = ex.as<double2>();
+  P.status = st.as<int>();
+  P.fail_t = ft.as<double>();
+  P.stats = stt.as<long long>();
+  P.jump_count = jc.as<int>();
+  P.jump_time = jt.as<double>();
+  P.jump_channel = jch.as<int>();
+  P.attempts_total = att.as<long long>();
+  cudaEventRecord(ctx->ev[2], s);
+  if ((ce = launch_batch(P, grid, s))) return cuda_fail(ce, "batch launch");
+  cudaEventRecord(ctx->ev[3], s);
+  o.expect.resize(nvals * n_sys);
+  o.status.resize(n_sys);
+  o.ftime.resize(n_sys);
+  o.stats.resize(3 * n_sys);
+  o.jcount.resize(n_sys);
+  o.jtime.resize(std::max<long long>(1, n_sys * jump_cap));
+  o.jch.resize(std::max<long long>(1, n_sys * jump_cap));
+  if ((ce = cudaMemcpyAsync(o.expect.data(), ex.p, nvals * n_sys * sizeof(double2), cudaMemcpyDeviceToHost, s)) ||
+      (ce = cudaMemcpyAsync(o.status.data(), st.p, sizeof(int) * n_sys, cudaMemcpyDeviceToHost, s)) ||
+      (ce = cudaMemcpyAsync(o.ftime.data(), ft.p, sizeof(double) * n_sys, cudaMemcpyDeviceToHost, s)) ||
+      (ce = cudaMemcpyAsync(o.stats.data(), stt.p, sizeof(long long) * 3 * n_sys, cudaMemcpyDeviceToHost, s)) ||
+      (ce = cudaMemcpyAsync(o.jcount.data(), jc.p, sizeof(int) * n_sys, cudaMemcpyDeviceToHost, s)) ||
+      (ce = cudaMemcpyAsync(o.jtime.data(), jt.p, sizeof(double) * o.jtime.size(), cudaMemcpyDeviceToHost, s)) ||
+      (ce = cudaMemcpyAsync(o.jch.data(), jch.p, sizeof(int) * o.jch.size(), cudaMemcpyDeviceToHost, s)) ||
+      (ce = cudaMemcpyAsync(&o.attempts, att.p, 8, cudaMemcpyDeviceToHost, s)) || (ce = cudaStreamSynchronize(s)))
+    return cuda_fail(ce, "batch solve");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+  o.kernel_ms = ms;
+  return QSG_OK;
+}
+
+qsg_status common_setup(qsg_ctx* ctx, const qsg_generator* G, long long n, const double* tlist, long long n_t,
+                        const qsg_solve_opts* opts, BatchProblem& P) {
+  if (!ctx) {
+    set_error("InvalidGrid: null context");
+    return QSG_INVALID_GRID;
+  }
+  cudaSetDevice(ctx->device);
+  if (qsg_status s = check_tlist(tlist, n_t)) return s;
+  if (qsg_status s = check_generator(G, n)) return s;
+  if (opts && opts->method != 0) {
+    set_error("InvalidGrid: only the adaptive Dormand-Prince 5(4) method runs on the device");
+    return QSG_UNSUPPORTED;
+  }
+  P.n = static_cast<int>(n);
+  P.gen = make_devgen(G);
+  P.atol = opts ? opts->abstol : 1e-8;
+  P.rtol = opts ? opts->reltol : 1e-6;
+  if (!(P.atol > 0 && P.rtol > 0)) {
+    set_error("InvalidGrid: tolerances must be positive");
+    return QSG_INVALID_GRID;
+  }
+  P.max_steps = opts ? opts->max_steps : 10000000LL;
+  P.n_t = static_cast<int>(n_t);
+  P.t0 = tlist[0];
+  P.tf = tlist[n_t - 1];
+  return QSG_OK;
+}
+
+}  // namespace
+
+extern "C" qsg_status qsg_mcsolve(qsg_ctx* ctx, const qsg_generator* G, int32_t n_c, const qsg_csr* c_ops,
+                                  int32_t n_e, const qsg_csr* e_ops, int64_t d, const double* psi0,
+                                  const double* tlist, int64_t n_t, const double* params, int32_t n_params,
+                                  uint64_t seed, int64_t traj_begin, int64_t traj_end, const qsg_solve_opts* opts,
+                                  qsg_mc_out* out, qsg_timing* timing) {
+  BatchProblem P{};
+  if (qsg_status s = common_setup(ctx, G, d, tlist, n_t, opts, P)) return s;
+  if (traj_end <= traj_begin) {
+    set_error("InvalidGrid: ntraj must be >= 1");
+    return QSG_INVALID_GRID;
+  }
+  if (n_c > kBatchMaxCops || n_e > kBatchMaxEops) {
+    set_error("TooLarge: mcsolve supports at most 32 collapse and 8 expectation operators");
+    return QSG_TOO_LARGE;
+  }
+  cudaStream_t s = ctx->stream;
+  cudaError_t ce;
+  P.mode = 0;
+  P.d = static_cast<int>(d);
+  P.eps_t = 1e-12 * std::max(1.0, std::fabs(P.tf));  // trajectories.cpp:130
+  P.seed = seed;
+  P.sys_begin = traj_begin;
+  TmpOps keep;
+  for (int k = 0; k < n_c; ++k) {
+    if (c_ops[k].n_rows != d || c_ops[k].n_cols != d) {
+      set_error("DimsMismatch: collapse operator dims mismatch");
+      return QSG_DIMS_MISMATCH;
+    }
+    if (qsg_status st = make_sell(ctx, c_ops[k], keep, P.c_ops[k])) return st;
+  }
+  for (int e = 0; e < n_e; ++e) {
+    if (e_ops[e].n_rows != d || e_ops[e].n_cols != d) {
+      set_error("DimsMismatch: e_op dims mismatch");
+      return QSG_DIMS_MISMATCH;
+    }
+    if (qsg_status st = make_sell(ctx, e_ops[e], keep, P.e_ops[e])) return st;
+  }
+  P.n_c = n_c;
+  P.n_e = n_e;
+  DevBuf dy0, dt, dp;
+  if ((ce = upload(dy0, psi0, sizeof(double2) * d, s)) || (ce = upload(dt, tlist, sizeof(double) * n_t, s)) ||
+      (n_params > 0 && (ce = upload(dp, params, sizeof(double) * n_params, s))))
+    return cuda_fail(ce, "mcsolve inputs");
+  P.y0 = dy0.as<double2>();
+  P.tlist = dt.as<double>();
+  P.params = n_params > 0 ? dp.as<double>() : nullptr;
+  P.n_params = n_params;
+  const long long nsys = traj_end - traj_begin;
+  const int cap = static_cast<int>(std::max<int64_t>(1, out ? out->jump_capacity : 1));
+  RunOut o;
+  if (qsg_status st = run_batch(ctx, P, nsys, std::max(cap, 64), o)) return st;
+  const int run_cap = std::max(cap, 64);
+  const size_t nv = static_cast<size_t>(n_e) * n_t;
+  std::vector<const double*> okm;
+  for (long long i = 0; i < nsys; ++i) {
+    const bool ok = o.status[i] == kDone;
+    if (out) {
+      if (out->failed) out->failed[i] = ok ? 0 : o.status[i];
+      if (out->fail_time) out->fail_time[i] = o.ftime[i];
+      if (out->traj_stats)
+        for (int k = 0; k < 3; ++k) out->traj_stats[3 * i + k] = o.stats[3 * i + k];
+      if (out->jump_count) out->jump_count[i] = o.jcount[i];
+      const double* jt = o.jtime.data() + i * run_cap;
+      const int* jc = o.jch.data() + i * run_cap;
+      RunOut o1;  // a jump log longer than the device buffer: re-run this trajectory alone
+      if (o.jcount[i] > run_cap && cap > run_cap) {
+        BatchProblem P1 = P;
+        P1.sys_begin = traj_begin + i;
+        if (qsg_status st = run_batch(ctx, P1, 1, o.jcount[i], o1)) return st;
+        jt = o1.jtime.data();
+        jc = o1.jch.data();
+      }
+      const int nstore = std::min(cap, o.jcount[i]);
+      for (int j = 0; j < nstore; ++j) {
+        if (out->jump_time) out->jump_time[i * cap + j] = jt[j];
+        if (out->jump_channel) out->jump_channel[i * cap + j] = jc[j];
+      }
+      if (out->per_traj_expect)
+        std::copy(reinterpret_cast<const double*>(o.expect.data() + i * nv),
+                  reinterpret_cast<const double*>(o.expect.data() + (i + 1) * nv), out->per_traj_expect + 2 * i * nv);
+    }
+    if (ok) okm.push_back(reinterpret_cast<const double*>(o.expect.data() + i * nv));
+  }
+  if (out && out->n_ok) *out->n_ok = static_cast<int64_t>(okm.size());
+  if (out && out->block_sum) {
+    if (okm.empty()) std::fill(out->block_sum, out->block_sum + 2 * nv, 0.0);
+    else pairwise(okm, 0, okm.size(), nv, out->block_sum);
+  }
+  if (timing) {
+    timing->kernel_ms = o.kernel_ms;
+    timing->attempts = o.attempts;
+    timing->grid_ctas = o.grid;
+    timing->lanes = batch_slots();
+  }
+  return QSG_OK;
+}
+
+extern "C" qsg_status qsg_mesolve_batch(qsg_ctx* ctx, const qsg_generator* L, int64_t d, const double* rho0,
+                                        const double* tlist, int64_t n_t, int32_t n_e, const qsg_csr* e_ops,
+                                        int64_t n_points, const double* params, int32_t n_params,
+                                        const qsg_solve_opts* opts, double* expect, qsg_stats* stats,
+                                        int32_t* status, qsg_timing* timing) {
+  BatchProblem P{};
+  if (qsg_status s = common_setup(ctx, L, d * d, tlist, n_t, opts, P)) return s;
+  if (n_points < 1) {
+    set_error("InvalidGrid: need at least one parameter point");
+    return QSG_INVALID_GRID;
+  }
+  if (n_e > kBatchMaxEops) {
+    set_error("TooLarge: at most 8 e_ops per sweep");
+    return QSG_TOO_LARGE;
+  }
+  cudaStream_t s = ctx->stream;
+  cudaError_t ce;
+  P.mode = 1;
+  P.d = static_cast<int>(d);
+  P.eps_t = 1e-12 * std::max({1.0, std::fabs(P.tf), std::fabs(P.t0)});  // evolve.cpp:128
+  std::vector<int> eo_off(1, 0), eo_i, eo_j;
+  std::vector<double> eo_v;
+  for (int e = 0; e < n_e; ++e) {
+    const qsg_csr& A = e_ops[e];
+    if (A.n_rows != d || A.n_cols != d) {
+      set_error("DimsMismatch: e_ops dims mismatch");
+      return QSG_DIMS_MISMATCH;
+    }
+    for (long long r = 0; r < A.n_rows; ++r)
+      for (int p = A.rowptr[r]; p < A.rowptr[r + 1]; ++p) {
+        eo_i.push_back(static_cast<int>(r));
+        eo_j.push_back(A.col[p]);
+        eo_v.push_back(A.val[2 * p]);
+        eo_v.push_back(A.val[2 * p + 1]);
+      }
+    eo_off.push_back(static_cast<int>(eo_i.size()));
+  }
+  DevBuf dy0, dt, dp, a, b, c, v;
+  if ((ce = upload(dy0, rho0, sizeof(double2) * d * d, s)) || (ce = upload(dt, tlist, sizeof(double) * n_t, s)) ||
+      (ce = upload(dp, params, sizeof(double) * std::max<long long>(1, n_points * n_params), s)) ||
+      (ce = upload(a, eo_off.data(), sizeof(int) * eo_off.size(), s)) ||
+      (ce = upload(b, eo_i.data(), sizeof(int) * eo_i.size(), s)) ||
+      (ce = upload(c, eo_j.data(), sizeof(int) * eo_j.size(), s)) ||
+      (ce = upload(v, eo_v.data(), sizeof(double) * eo_v.size(), s)))
+    return cuda_fail(ce, "sweep inputs");
+  P.y0 = dy0.as<double2>();
+  P.tlist = dt.as<double>();
+  P.params = n_params > 0 ? dp.as<double>() : nullptr;
+  P.n_params = n_params;
+  P.n_e = n_e;
+  P.eo_off = a.as<int>();
+  P.eo_i = b.as<int>();
+  P.eo_j = c.as<int>();
+  P.eo_v = v.as<double2>();
+  P.sys_begin = 0;
+  RunOut o;
+  if (qsg_status st = run_batch(ctx, P, n_points, 1, o)) return st;
+  const size_t nv = static_cast<size_t>(n_e) * n_t;
+  qsg_status rc = QSG_OK;
+  for (long long i = 0; i < n_points; ++i) {
+    if (expect)
+      std::copy(reinterpret_cast<const double*>(o.expect.data() + i * nv),
+                reinterpret_cast<const double*>(o.expect.data() + (i + 1) * nv), expect + 2 * i * nv);
+    if (stats) stats[i] = qsg_stats{o.stats[3 * i], o.stats[3 * i + 1], o.stats[3 * i + 2]};
+    if (status) status[i] = o.status[i] == kDone ? 0 : QSG_INTEGRATION_FAILURE;
+    if (o.status[i] != kDone && rc == QSG_OK) rc = status_from_device(o.status[i], o.ftime[i]);
+  }
+  if (timing) {
+    timing->kernel_ms = o.kernel_ms;
+    timing->attempts = o.attempts;
+    timing->grid_ctas = o.grid;
+    timing->lanes = batch_slots();
+  }
+  return status ? QSG_OK : rc;
+}

@@ -1,20 +1,747 @@
-// Batched trajectory / sweep engine — entry points (implementation in progress).
-#include "qsg_internal.h"
+// Batched Dormand-Prince 5(4) engine for many independent systems: Monte-Carlo trajectories
+// (mcsolve, trajectories.cpp:106-249) and parameter-sweep points (one mesolve per point).
+//
+// Each CTA owns B = 8 "slots"; the state vectors of its slots are interleaved as [n][B] so that
+// lane l of a warp works on (row = 4*warp_iter + l/8, slot = l%8): a CSR entry of a row is
+// loaded once and broadcast to the 8 slots, and the gather x[col] of the 8 slots is one
+// contiguous 128 B line. Slots run their own integrator state machines in lock-step "rounds"
+// of passes; a finished slot pulls the next system from a global queue (dynamic load balance),
+// trajectory i always drawing from RngStream(seed, i) (trajectories.cpp:42), so results do not
+// depend on the CTA, slot or GPU count that ran them.
+//
+// Round (per slot phase):            P1        P2          P3        P4..P5  P6        P7
+//   START  (start + initial_step)    k1,d0,d1  k2,d2       -         -       -         -
+//   RUN    (one DP5 attempt)         stage 2   stage 3     stage 4   5, 6    7 + err   commit/Gram
+//   JUMP   (trajectories.cpp:177-203) obs+wts  collapse    restart   -       -         -
+//   OBS / FINISH                     obs       -           -         -       -         -
+// Jump location: |psi(theta)|^2 of the dense output is a polynomial whose coefficients come from
+// the Gram matrix of rc1..rc5 (one fused reduction in P7); the reference's <=200-step bisection
+// (trajectories.cpp:156-168) then runs on scalars in every thread of the slot.
+#include <cstdio>
 
-using namespace qsg;
+#include "batch_engine.h"
+#include "engine.cuh"
 
-extern "C" qsg_status qsg_mcsolve(qsg_ctx*, const qsg_generator*, int32_t, const qsg_csr*, int32_t,
-                                  const qsg_csr*, int64_t, const double*, const double*, int64_t,
-                                  const double*, int32_t, uint64_t, int64_t, int64_t,
-                                  const qsg_solve_opts*, qsg_mc_out*, qsg_timing*) {
-  set_error("mcsolve engine not built yet");
-  return QSG_UNSUPPORTED;
+namespace qsg {
+
+namespace {
+
+constexpr int B = 8;            // slots per CTA
+constexpr int kThreads = 512;   // 16 warps
+constexpr int W = kThreads / 32;
+constexpr int RPW = 32 / B;     // rows per warp iteration
+constexpr int NBUF = 14;
+
+enum Buf { Y = 0, YO, K1, K1O, K2, K3, K4, K5, K6, K7, SA, SB, Y1, SC };
+enum Phase { FREE = 0, START, RUN, JUMP, OBS, FINISH, DONE };
+enum Src { SRC_DENSE = 0, SRC_Y = 1, SRC_SC = 2 };
+
+struct Slot {
+  int phase, next_phase, after_obs;
+  long long sys;  // index relative to sys_begin
+  int status;
+  double t, t_old, h, h_last, facold, h0, hh;
+  int clamped, attempts, accepted, crossing, fresh;
+  long long steps, rejected, rhs_evals;
+  unsigned long long rng[4];
+  double r, jump_t, d0, d1;
+  int channel, njumps, grid;
+  double obs_limit;  // grid points <= obs_limit + eps_t are observed from the dense output
+  int tail_src;      // -1, or the direct source that takes every later grid point
+  int n_pend;
+  double pend_theta[kBatchMaxPend];
+  int pend_grid[kBatchMaxPend];
+  int pend_src[kBatchMaxPend];
+  double w[kBatchMaxCops];
+  double gram[15];
+  double nrm2, err;
+};
+
+__device__ __forceinline__ unsigned long long rotl64(unsigned long long x, int k) {
+  return (x << k) | (x >> (64 - k));
+}
+__device__ void rng_init(unsigned long long* s, unsigned long long seed, unsigned long long stream) {
+  unsigned long long z = seed ^ ((stream + 1) * 0x9E3779B97F4A7C15ULL);  // rng.cpp:21-25
+  for (int i = 0; i < 4; ++i) {
+    unsigned long long x = (z += 0x9E3779B97F4A7C15ULL);
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    s[i] = x ^ (x >> 31);
+  }
+  if ((s[0] | s[1] | s[2] | s[3]) == 0) s[0] = 1;
+}
+__device__ unsigned long long rng_next(unsigned long long* s) {  // rng.cpp:27-37
+  const unsigned long long result = rotl64(s[0] + s[3], 23) + s[0];
+  const unsigned long long t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = rotl64(s[3], 45);
+  return result;
+}
+__device__ double rng_uniform(unsigned long long* s) { return static_cast<double>(rng_next(s) >> 11) * 0x1.0p-53; }
+__device__ double rng_uniform_pos(unsigned long long* s) {
+  double u = rng_uniform(s);
+  while (u == 0.0) u = rng_uniform(s);
+  return u;
 }
 
-extern "C" qsg_status qsg_mesolve_batch(qsg_ctx*, const qsg_generator*, int64_t, const double*,
-                                        const double*, int64_t, int32_t, const qsg_csr*, int64_t,
-                                        const double*, int32_t, const qsg_solve_opts*, double*,
-                                        qsg_stats*, int32_t*, qsg_timing*) {
-  set_error("batched mesolve engine not built yet");
-  return QSG_UNSUPPORTED;
+struct Ctx {
+  const BatchProblem& P;
+  double2* w;  // CTA workspace
+  int n;
+  __device__ double2* buf(int k) const { return w + static_cast<long long>(k) * n * B; }
+  __device__ double2 ld(int k, int r, int s) const { return buf(k)[static_cast<long long>(r) * B + s]; }
+  __device__ void st(int k, int r, int s, double2 v) const { buf(k)[static_cast<long long>(r) * B + s] = v; }
+};
+
+// dense output of slot s at index c (integrator.hpp:127-131,150-154) from the committed step
+__device__ __forceinline__ double2 dense_at(const Ctx& C, int c, int s, double theta, double h, int src) {
+  if (src == SRC_Y) return C.ld(Y, c, s);
+  if (src == SRC_SC) return C.ld(SC, c, s);
+  using namespace dp;
+  const double2 yo = C.ld(YO, c, s), y1 = C.ld(Y, c, s), k1 = C.ld(K1O, c, s), k7 = C.ld(K7, c, s);
+  const double2 k3 = C.ld(K3, c, s), k4 = C.ld(K4, c, s), k5 = C.ld(K5, c, s), k6 = C.ld(K6, c, s);
+  const double th1 = 1.0 - theta;
+  const double2 rc2 = csub(y1, yo);
+  const double2 rc3 = csub(cscale(h, k1), rc2);
+  const double2 rc4 = csub(csub(rc2, cscale(h, k7)), rc3);
+  double2 rc5;
+  rc5.x = h * (d1 * k1.x + d3 * k3.x + d4 * k4.x + d5 * k5.x + d6 * k6.x + d7 * k7.x);
+  rc5.y = h * (d1 * k1.y + d3 * k3.y + d4 * k4.y + d5 * k5.y + d6 * k6.y + d7 * k7.y);
+  double2 o;
+  o.x = yo.x + theta * (rc2.x + th1 * (rc3.x + theta * (rc4.x + th1 * rc5.x)));
+  o.y = yo.y + theta * (rc2.y + th1 * (rc3.y + theta * (rc4.y + th1 * rc5.y)));
+  return o;
 }
+
+// one row of a SELL operator applied to slot s of a gathered vector
+template <class XF>
+__device__ __forceinline__ double2 sell_row_slot(const DevSell& A, int row, XF&& xf) {
+  const int sl = row >> 5, ln = row & 31;
+  const int len = __ldg(A.rowlen + row);
+  const long long base = __ldg(A.slice_off + sl) * 32 + ln;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int j = 0; j < len; j += 4) {
+    int c[4];
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (j + u < len) {
+        c[u] = __ldg(A.col + base + 32LL * (j + u));
+        v[u] = __ldg(A.val + base + 32LL * (j + u));
+      } else {
+        c[u] = 0;
+        v[u] = make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (j + u < len) cfma(v[u], xf(c[u]), acc);
+  }
+  return acc;
+}
+
+template <class XF>
+__device__ __forceinline__ double2 gen_row_slot(const DevGen& g, const double* params, int row, double t,
+                                                XF&& xf) {
+  double2 s = sell_row_slot(g.A[0], row, xf);
+  for (int k = 1; k < g.n_terms; ++k) {
+    const double2 sk = sell_row_slot(g.A[k], row, xf);
+    s = cadd(s, cmul(coeff_eval(g.c[k], params, t), sk));
+  }
+  return s;
+}
+
+// Deterministic per-slot reduction of NA accumulators: out[slot*NA + a] (shared memory).
+template <int NA>
+__device__ void slot_reduce(double (&acc)[NA], double* sred, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, s = lane % B, rs = lane / B;
+#pragma unroll
+  for (int a = 0; a < NA; ++a)
+#pragma unroll
+    for (int off = B; off < 32; off <<= 1) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], off);
+  if (rs == 0)
+#pragma unroll
+    for (int a = 0; a < NA; ++a) sred[(warp * B + s) * NA + a] = acc[a];
+  __syncthreads();
+  if (threadIdx.x < B * NA) {
+    const int ss = threadIdx.x / NA, a = threadIdx.x % NA;
+    double v = 0.0;
+    for (int w = 0; w < W; ++w) v += sred[(w * B + ss) * NA + a];
+    out[ss * NA + a] = v;
+  }
+  __syncthreads();
+}
+
+__device__ double params_at(const BatchProblem& P, const Slot& S, int i) {
+  return P.mode == 1 ? P.params[(P.sys_begin + S.sys) * P.n_params + i] : P.params[i];
+}
+
+// per-slot parameter pointer for generator coefficients
+__device__ __forceinline__ const double* slot_params(const BatchProblem& P, const Slot& S) {
+  if (!P.params) return nullptr;
+  return P.mode == 1 ? P.params + (P.sys_begin + S.sys) * P.n_params : P.params;
+}
+
+// Queue the next grid points of a slot: dense-output points first (<= obs_limit + eps_t), then,
+// if a tail source is set, every remaining point from that direct state.
+__device__ void refill(Slot& s, const BatchProblem& P) {
+  while (s.n_pend < kBatchMaxPend && s.grid < P.n_t) {
+    if (P.tlist[s.grid] <= s.obs_limit + P.eps_t) {
+      s.pend_theta[s.n_pend] = (fmin(P.tlist[s.grid], s.t) - s.t_old) / s.h_last;
+      s.pend_src[s.n_pend] = SRC_DENSE;
+    } else if (s.tail_src >= 0) {
+      s.pend_theta[s.n_pend] = 0.0;
+      s.pend_src[s.n_pend] = s.tail_src;
+    } else {
+      break;
+    }
+    s.pend_grid[s.n_pend] = s.grid;
+    ++s.n_pend;
+    ++s.grid;
+  }
+}
+__device__ bool has_more(const Slot& s, const BatchProblem& P) {
+  return s.grid < P.n_t && (P.tlist[s.grid] <= s.obs_limit + P.eps_t || s.tail_src >= 0);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constant__ BatchProblem P) {
+  __shared__ Slot S[B];
+  __shared__ double sred[W * B * 15];
+  __shared__ double sout[B * 15];
+  __shared__ int s_alldone;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sl = lane % B, rs = lane / B;
+  const int n = P.n;
+  const Ctx C{P, P.work + static_cast<long long>(blockIdx.x) * P.work_stride, n};
+  const double atol = P.atol, rtol = P.rtol, eps_t = P.eps_t, tf = P.tf, t0 = P.t0;
+  auto rows = [&](auto&& f) {
+    for (int r = warp * RPW + rs; r < n; r += W * RPW) f(r);
+  };
+
+  if (threadIdx.x < B) {
+    S[threadIdx.x].phase = FREE;
+    S[threadIdx.x].next_phase = FREE;
+  }
+  __syncthreads();
+
+  for (;;) {
+    // ---------------- slot bookkeeping (one thread per slot) ----------------
+    if (threadIdx.x < B) {
+      Slot& s = S[threadIdx.x];
+      s.fresh = 0;
+      if (s.phase == FREE) {
+        const unsigned long long idx = atomicAdd(P.queue, 1ull);
+        if (idx < static_cast<unsigned long long>(P.n_systems)) {
+          s.sys = static_cast<long long>(idx);
+          s.phase = START;
+          s.fresh = 1;
+          s.status = kRunning;
+          s.t = s.t_old = t0;
+          s.h = s.h_last = 0.0;
+          s.facold = 1e-4;
+          s.steps = s.rejected = s.rhs_evals = 0;
+          s.attempts = 0;
+          s.njumps = 0;
+          s.grid = 0;
+          s.n_pend = 0;
+          s.obs_limit = -1e300;
+          s.tail_src = -1;
+          // events at t0 observe y0 directly (evolve.cpp:134-137, trajectories.cpp:142)
+          if (P.mode == 0) {
+            s.pend_theta[0] = 0.0;
+            s.pend_grid[0] = 0;
+            s.pend_src[0] = SRC_Y;
+            s.n_pend = 1;
+            s.grid = 1;
+            rng_init(s.rng, P.seed, static_cast<unsigned long long>(P.sys_begin + s.sys));
+            s.r = rng_uniform_pos(s.rng);  // trajectories.cpp:144
+          } else {
+            while (s.grid < P.n_t && P.tlist[s.grid] <= t0 + eps_t && s.n_pend < kBatchMaxPend) {
+              s.pend_theta[s.n_pend] = 0.0;
+              s.pend_grid[s.n_pend] = s.grid;
+              s.pend_src[s.n_pend] = SRC_Y;
+              ++s.n_pend;
+              ++s.grid;
+            }
+          }
+        } else {
+          s.phase = DONE;
+        }
+      }
+      s.next_phase = s.phase;
+      if (s.phase == RUN) {
+        // Dopri5::step prologue (integrator.hpp:80-89) and the max_steps guard (:157-159)
+        if (s.attempts == 0 && s.steps >= P.max_steps) {
+          s.status = kFailMaxSteps;
+        } else {
+          s.hh = fmin(s.h, tf - s.t);
+          s.clamped = s.hh < s.h;
+          if (!(s.hh > 0.0)) s.status = kFailPastEnd;
+          else if (s.hh <= fabs(s.t) * 1e-15 + 1e-300) s.status = kFailUnderflow;
+          else if (++s.attempts > 1000) s.status = kFailRejected;
+        }
+        if (s.status != kRunning) {
+          s.phase = FINISH;
+          s.n_pend = 0;
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
+      int all = 1;
+      for (int b = 0; b < B; ++b) all &= (S[b].phase == DONE);
+      s_alldone = all;
+    }
+    __syncthreads();
+    if (s_alldone) break;
+    const int ph = S[sl].phase;
+
+    // fresh slots: y <- y0
+    rows([&](int r) {
+      if (S[sl].fresh) C.st(Y, r, sl, P.y0[r]);
+    });
+    __syncthreads();
+
+    // ================= P1 =================
+    {
+      double acc[2] = {0.0, 0.0};
+      const double* prm = slot_params(P, S[sl]);
+      if (ph == START) {
+        rows([&](int r) {
+          const double2 k = gen_row_slot(P.gen, prm, r, t0, [&](int c) { return C.ld(Y, c, sl); });
+          C.st(K1, r, sl, k);
+          const double2 yy = C.ld(Y, r, sl);
+          const double sc = atol + rtol * cabs_(yy);
+          acc[0] += cnorm(make_double2(yy.x / sc, yy.y / sc));
+          acc[1] += cnorm(make_double2(k.x / sc, k.y / sc));
+        });
+      } else if (ph == RUN) {
+        const double hh = S[sl].hh, t = S[sl].t;
+        using namespace dp;
+        rows([&](int r) {
+          const double2 k = gen_row_slot(P.gen, prm, r, t + c2 * hh, [&](int c) {
+            const double2 a = C.ld(Y, c, sl), q = C.ld(K1, c, sl);
+            return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
+          });
+          const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl);
+          C.st(K2, r, sl, k);
+          C.st(SA, r, sl, make_double2(yy.x + hh * (a31 * q1.x + a32 * k.x), yy.y + hh * (a31 * q1.y + a32 * k.y)));
+        });
+      }
+      slot_reduce<2>(acc, sred, sout);
+      if (threadIdx.x < B && S[threadIdx.x].phase == START) {
+        Slot& s = S[threadIdx.x];
+        s.d0 = sqrt(sout[threadIdx.x * 2] / static_cast<double>(n));
+        s.d1 = sqrt(sout[threadIdx.x * 2 + 1] / static_cast<double>(n));
+        double h0 = (s.d0 < 1e-5 || s.d1 < 1e-5) ? 1e-6 : 0.01 * s.d0 / s.d1;  // integrator.hpp:168-170
+        h0 = fmin(h0, tf - s.t);
+        if (!(h0 > 0)) h0 = 1e-6;
+        s.h0 = h0;
+        s.rhs_evals += 1;
+      }
+      // ---- pending observations (every phase may carry some)
+      int maxp = 0;
+      for (int b = 0; b < B; ++b) maxp = max(maxp, S[b].phase == DONE ? 0 : S[b].n_pend);
+      for (int q = 0; q < maxp; ++q) {
+        const bool act = q < S[sl].n_pend && S[sl].phase != DONE;
+        const double th = act ? S[sl].pend_theta[q] : 0.0;
+        const int src = act ? S[sl].pend_src[q] : SRC_Y;
+        const double hl = S[sl].h_last;
+        for (int e = 0; e < P.n_e; ++e) {
+          double oa[3] = {0.0, 0.0, 0.0};
+          if (act) {
+            if (P.mode == 0) {  // <g|E g> / |g|^2 (trajectories.cpp:133-139)
+              rows([&](int r) {
+                const double2 ev = sell_row_slot(P.e_ops[e], r, [&](int c) { return dense_at(C, c, sl, th, hl, src); });
+                const double2 g = dense_at(C, r, sl, th, hl, src);
+                const double2 p = cmul(cconj(g), ev);
+                oa[0] += p.x;
+                oa[1] += p.y;
+                oa[2] += cnorm(g);
+              });
+            } else {  // sum A(i,j) rho_h(j,i) (evolve.cpp:286-295)
+              const int beg = P.eo_off[e], end = P.eo_off[e + 1];
+              for (int p = beg + warp * RPW + rs; p < end; p += W * RPW) {
+                const int i = P.eo_i[p], j = P.eo_j[p];
+                const double2 rji = dense_at(C, i * P.d + j, sl, th, hl, src);
+                const double2 rij = dense_at(C, j * P.d + i, sl, th, hl, src);
+                const double2 v = cmul(P.eo_v[p], cscale(0.5, cadd(rji, cconj(rij))));
+                oa[0] += v.x;
+                oa[1] += v.y;
+              }
+            }
+          }
+          slot_reduce<3>(oa, sred, sout);
+          if (threadIdx.x < B && q < S[threadIdx.x].n_pend && S[threadIdx.x].phase != DONE) {
+            Slot& s = S[threadIdx.x];
+            double2 v = make_double2(sout[threadIdx.x * 3], sout[threadIdx.x * 3 + 1]);
+            if (P.mode == 0) {
+              const double inv = 1.0 / sout[threadIdx.x * 3 + 2];
+              v = make_double2(v.x * inv, v.y * inv);
+            }
+            P.expect[s.sys * P.n_e * P.n_t + static_cast<long long>(s.pend_grid[q]) * P.n_e + e] = v;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- jump weights |C_k g(jump_t)|^2 (trajectories.cpp:178-196), chunks of 8 channels
+      if (P.mode == 0) {
+        bool anyj = false;
+        for (int b = 0; b < B; ++b) anyj |= (S[b].phase == JUMP);
+        if (anyj) {
+          const double thj = (S[sl].jump_t - S[sl].t_old) / S[sl].h_last, hl = S[sl].h_last;
+          for (int k0 = 0; k0 < P.n_c; k0 += 8) {
+            double wa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (ph == JUMP) {
+              rows([&](int r) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                  if (k0 + u < P.n_c) {
+                    const double2 v = sell_row_slot(P.c_ops[k0 + u], r,
+                                                    [&](int c) { return dense_at(C, c, sl, thj, hl, SRC_DENSE); });
+                    wa[u] += cnorm(v);
+                  }
+              });
+            }
+            slot_reduce<8>(wa, sred, sout);
+            if (threadIdx.x < B && S[threadIdx.x].phase == JUMP)
+              for (int u = 0; u < 8 && k0 + u < P.n_c; ++u) S[threadIdx.x].w[k0 + u] = sout[threadIdx.x * 8 + u];
+          }
+          __syncthreads();
+          if (threadIdx.x < B && S[threadIdx.x].phase == JUMP) {
+            Slot& s = S[threadIdx.x];
+            double total = 0.0;
+            for (int k = 0; k < P.n_c; ++k) total += s.w[k];
+            if (total <= 0.0) {
+              s.status = kFailJumpWeights;
+              s.next_phase = FINISH;
+            } else {
+              const double u = rng_uniform(s.rng) * total;
+              int ch = 0;
+              double a = 0.0;
+              for (; ch < P.n_c; ++ch) {
+                a += s.w[ch];
+                if (u < a) break;
+              }
+              if (ch == P.n_c) ch = P.n_c - 1;
+              s.channel = ch;
+              if (s.njumps < P.jump_cap) {
+                P.jump_time[s.sys * P.jump_cap + s.njumps] = s.jump_t;
+                P.jump_channel[s.sys * P.jump_cap + s.njumps] = ch;
+              }
+              ++s.njumps;
+              s.r = rng_uniform_pos(s.rng);  // trajectories.cpp:201
+            }
+          }
+        }
+      }
+      if (threadIdx.x < B) {
+        Slot& s = S[threadIdx.x];
+        if (s.phase != DONE) s.n_pend = 0;
+      }
+      __syncthreads();
+    }
+
+    // ================= P2 =================
+    {
+      double acc[1] = {0.0};
+      const double* prm = slot_params(P, S[sl]);
+      const int ph2 = S[sl].phase;
+      if (ph2 == START) {
+        const double h0 = S[sl].h0;
+        rows([&](int r) {
+          const double2 k = gen_row_slot(P.gen, prm, r, t0 + h0, [&](int c) {
+            const double2 a = C.ld(Y, c, sl), q = C.ld(K1, c, sl);
+            return make_double2(a.x + h0 * q.x, a.y + h0 * q.y);
+          });
+          const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl);
+          const double sc = atol + rtol * cabs_(yy);
+          const double2 df = csub(k, q1);
+          acc[0] += cnorm(make_double2(df.x / sc, df.y / sc));
+        });
+      } else if (ph2 == RUN) {
+        const double hh = S[sl].hh, t = S[sl].t;
+        using namespace dp;
+        rows([&](int r) {
+          const double2 k = gen_row_slot(P.gen, prm, r, t + c3 * hh, [&](int c) { return C.ld(SA, c, sl); });
+          const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl);
+          C.st(K3, r, sl, k);
+          C.st(SB, r, sl, make_double2(yy.x + hh * (a41 * q1.x + a42 * q2.x + a43 * k.x),
+                                       yy.y + hh * (a41 * q1.y + a42 * q2.y + a43 * k.y)));
+        });
+      } else if (ph2 == JUMP && S[sl].next_phase == JUMP) {
+        // collapse: psi <- C_ch g / |C_ch g| (trajectories.cpp:198-199)
+        const double thj = (S[sl].jump_t - S[sl].t_old) / S[sl].h_last, hl = S[sl].h_last;
+        const int ch = S[sl].channel;
+        const double nrm = sqrt(S[sl].w[ch]);
+        rows([&](int r) {
+          const double2 v = sell_row_slot(P.c_ops[ch], r, [&](int c) { return dense_at(C, c, sl, thj, hl, SRC_DENSE); });
+          C.st(SC, r, sl, make_double2(v.x / nrm, v.y / nrm));
+        });
+      }
+      slot_reduce<1>(acc, sred, sout);
+      if (threadIdx.x < B && S[threadIdx.x].phase == START) {
+        Slot& s = S[threadIdx.x];
+        const double d2 = sqrt(sout[threadIdx.x] / static_cast<double>(n)) / s.h0;  // integrator.hpp:180-186
+        double h1;
+        if (fmax(s.d1, d2) <= 1e-15) h1 = fmax(1e-6, s.h0 * 1e-3);
+        else h1 = pow(0.01 / fmax(s.d1, d2), 0.2);
+        s.h = fmin(fmin(100.0 * s.h0, h1), tf - s.t);
+        s.rhs_evals += 1;
+        s.next_phase = RUN;
+      }
+      __syncthreads();
+    }
+
+    // ================= P3 =================
+    {
+      const double* prm = slot_params(P, S[sl]);
+      const int ph3 = S[sl].phase;
+      if (ph3 == RUN) {
+        const double hh = S[sl].hh, t = S[sl].t;
+        using namespace dp;
+        rows([&](int r) {
+          const double2 k = gen_row_slot(P.gen, prm, r, t + c4 * hh, [&](int c) { return C.ld(SB, c, sl); });
+          const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl), q3 = C.ld(K3, r, sl);
+          C.st(K4, r, sl, k);
+          C.st(SA, r, sl, make_double2(yy.x + hh * (a51 * q1.x + a52 * q2.x + a53 * q3.x + a54 * k.x),
+                                       yy.y + hh * (a51 * q1.y + a52 * q2.y + a53 * q3.y + a54 * k.y)));
+        });
+      } else if (ph3 == JUMP && S[sl].next_phase == JUMP && S[sl].jump_t < tf - eps_t) {
+        // restart: integ.start(jump_t, psi, tf, h_current) (trajectories.cpp:202-203)
+        const double tj = S[sl].jump_t;
+        rows([&](int r) {
+          const double2 k = gen_row_slot(P.gen, prm, r, tj, [&](int c) { return C.ld(SC, c, sl); });
+          C.st(K1, r, sl, k);
+          C.st(Y, r, sl, C.ld(SC, r, sl));
+        });
+      }
+      __syncthreads();
+      if (threadIdx.x < B && S[threadIdx.x].phase == JUMP && S[threadIdx.x].next_phase == JUMP) {
+        Slot& s = S[threadIdx.x];
+        if (s.jump_t < tf - eps_t) {
+          s.t = s.t_old = s.jump_t;
+          s.facold = 1e-4;
+          s.rhs_evals += 1;
+          s.attempts = 0;
+          s.next_phase = RUN;
+        } else {  // trajectories.cpp:204-206: fill the rest of the grid with the jumped state
+          s.obs_limit = -1e300;
+          s.tail_src = SRC_SC;
+          refill(s, P);
+          s.next_phase = has_more(s, P) ? OBS : FINISH;
+          s.after_obs = FINISH;
+        }
+      }
+      __syncthreads();
+    }
+
+    // ================= P4, P5 =================
+    if (S[sl].phase == RUN) {
+      const double* prm = slot_params(P, S[sl]);
+      const double hh = S[sl].hh, t = S[sl].t;
+      using namespace dp;
+      rows([&](int r) {
+        const double2 k = gen_row_slot(P.gen, prm, r, t + c5 * hh, [&](int c) { return C.ld(SA, c, sl); });
+        const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl), q3 = C.ld(K3, r, sl),
+                      q4 = C.ld(K4, r, sl);
+        C.st(K5, r, sl, k);
+        C.st(SB, r, sl,
+             make_double2(yy.x + hh * (a61 * q1.x + a62 * q2.x + a63 * q3.x + a64 * q4.x + a65 * k.x),
+                          yy.y + hh * (a61 * q1.y + a62 * q2.y + a63 * q3.y + a64 * q4.y + a65 * k.y)));
+      });
+    }
+    __syncthreads();
+    if (S[sl].phase == RUN) {
+      const double* prm = slot_params(P, S[sl]);
+      const double hh = S[sl].hh, t = S[sl].t;
+      using namespace dp;
+      rows([&](int r) {
+        const double2 k = gen_row_slot(P.gen, prm, r, t + hh, [&](int c) { return C.ld(SB, c, sl); });
+        const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q3 = C.ld(K3, r, sl), q4 = C.ld(K4, r, sl),
+                      q5 = C.ld(K5, r, sl);
+        C.st(K6, r, sl, k);
+        C.st(Y1, r, sl,
+             make_double2(yy.x + hh * (a71 * q1.x + a73 * q3.x + a74 * q4.x + a75 * q5.x + a76 * k.x),
+                          yy.y + hh * (a71 * q1.y + a73 * q3.y + a74 * q4.y + a75 * q5.y + a76 * k.y)));
+      });
+    }
+    __syncthreads();
+
+    // ================= P6: stage 7 + embedded error =================
+    {
+      double acc[2] = {0.0, 0.0};
+      if (S[sl].phase == RUN) {
+        const double* prm = slot_params(P, S[sl]);
+        const double hh = S[sl].hh, t = S[sl].t;
+        using namespace dp;
+        rows([&](int r) {
+          const double2 k = gen_row_slot(P.gen, prm, r, t + hh, [&](int c) { return C.ld(Y1, c, sl); });
+          const double2 yy = C.ld(Y, r, sl), y1 = C.ld(Y1, r, sl), q1 = C.ld(K1, r, sl), q3 = C.ld(K3, r, sl),
+                        q4 = C.ld(K4, r, sl), q5 = C.ld(K5, r, sl), q6 = C.ld(K6, r, sl);
+          C.st(K7, r, sl, k);
+          double2 e;
+          e.x = hh * (e1 * q1.x + e3 * q3.x + e4 * q4.x + e5 * q5.x + e6 * q6.x + e7 * k.x);
+          e.y = hh * (e1 * q1.y + e3 * q3.y + e4 * q4.y + e5 * q5.y + e6 * q6.y + e7 * k.y);
+          const double sc = atol + rtol * fmax(cabs_(yy), cabs_(y1));
+          const double qq = cabs_(e) / sc;
+          acc[0] += qq * qq;
+          acc[1] += cnorm(y1);
+        });
+      }
+      slot_reduce<2>(acc, sred, sout);
+      if (threadIdx.x < B && S[threadIdx.x].phase == RUN) {
+        Slot& s = S[threadIdx.x];
+        using namespace dp;
+        double err = sqrt(sout[threadIdx.x * 2] / static_cast<double>(n));
+        if (!isfinite(err)) err = 10.0;
+        s.nrm2 = sout[threadIdx.x * 2 + 1];
+        s.rhs_evals += 6;
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.attempts_total), 1ull);
+        if (err <= 1.0) {  // integrator.hpp:119-142
+          const double fac11 = pow(err, expo1);
+          double fac = fac11 / pow(s.facold, beta);
+          fac = fmax(facc2, fmin(facc1, fac / safe));
+          const double h_new = s.hh / fac;
+          s.facold = fmax(err, 1e-4);
+          s.t_old = s.t;
+          s.t += s.hh;
+          s.h_last = s.hh;
+          ++s.steps;
+          if (!s.clamped) s.h = h_new;
+          else s.h = fmax(s.h, h_new);
+          s.attempts = 0;
+          s.accepted = 1;
+          s.crossing = (P.mode == 0 && P.n_c > 0 && s.nrm2 < s.r) ? 1 : 0;  // trajectories.cpp:154
+        } else {
+          ++s.rejected;
+          s.h = s.hh / fmin(facc1, pow(err, expo1) / safe);  // integrator.hpp:144-145
+          s.accepted = 0;
+          s.crossing = 0;
+        }
+      }
+      __syncthreads();
+    }
+
+    // ================= P7: commit + Gram of the dense-output basis =================
+    {
+      double g[15];
+#pragma unroll
+      for (int a = 0; a < 15; ++a) g[a] = 0.0;
+      const bool acc_ok = S[sl].phase == RUN && S[sl].accepted;
+      const bool cross = acc_ok && S[sl].crossing;
+      if (acc_ok) {
+        const double h = S[sl].h_last;
+        using namespace dp;
+        rows([&](int r) {
+          const double2 yo = C.ld(Y, r, sl), y1 = C.ld(Y1, r, sl), k1 = C.ld(K1, r, sl), k7 = C.ld(K7, r, sl);
+          if (cross) {
+            const double2 k3 = C.ld(K3, r, sl), k4 = C.ld(K4, r, sl), k5 = C.ld(K5, r, sl), k6 = C.ld(K6, r, sl);
+            double2 rc[5];
+            rc[0] = yo;
+            rc[1] = csub(y1, yo);
+            rc[2] = csub(cscale(h, k1), rc[1]);
+            rc[3] = csub(csub(rc[1], cscale(h, k7)), rc[2]);
+            rc[4].x = h * (d1 * k1.x + d3 * k3.x + d4 * k4.x + d5 * k5.x + d6 * k6.x + d7 * k7.x);
+            rc[4].y = h * (d1 * k1.y + d3 * k3.y + d4 * k4.y + d5 * k5.y + d6 * k6.y + d7 * k7.y);
+            int q = 0;
+#pragma unroll
+            for (int a = 0; a < 5; ++a)
+#pragma unroll
+              for (int b = a; b < 5; ++b) g[q++] += rc[a].x * rc[b].x + rc[a].y * rc[b].y;  // Re <rc_a, rc_b>
+          }
+          C.st(K1O, r, sl, k1);
+          C.st(YO, r, sl, yo);
+          C.st(Y, r, sl, y1);
+          C.st(K1, r, sl, k7);
+        });
+      }
+      bool anyc = false;
+      for (int b = 0; b < B; ++b) anyc |= (S[b].phase == RUN && S[b].accepted && S[b].crossing);
+      if (anyc) slot_reduce<15>(g, sred, sout);
+      else __syncthreads();
+      if (threadIdx.x < B && S[threadIdx.x].phase == RUN && S[threadIdx.x].accepted) {
+        Slot& s = S[threadIdx.x];
+        double jt = s.t;
+        if (s.crossing) {
+          for (int a = 0; a < 15; ++a) s.gram[a] = sout[threadIdx.x * 15 + a];
+          // bisection on |psi(mid)|^2 - r (trajectories.cpp:156-168)
+          double lo = s.t_old, hi = s.t;
+          for (int it = 0; it < 200; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            const double th = (mid - s.t_old) / s.h_last, t1 = 1.0 - th;
+            const double wv[5] = {1.0, th, th * t1, th * th * t1, th * th * t1 * t1};
+            double nn = 0.0;
+            int q = 0;
+            for (int a = 0; a < 5; ++a)
+              for (int b = a; b < 5; ++b, ++q) nn += (a == b ? 1.0 : 2.0) * wv[a] * wv[b] * s.gram[q];
+            const double gg = nn - s.r;
+            if (fabs(gg) < 1e-10) {
+              lo = hi = mid;
+              break;
+            }
+            if (gg > 0) lo = mid;
+            else hi = mid;
+          }
+          jt = 0.5 * (lo + hi);
+          s.jump_t = jt;
+        }
+        // observation events reached by this step (evolve.cpp:160-165 / trajectories.cpp:171-175);
+        // after the last step the trailing grid points take the final state directly (:169, :207-208)
+        s.n_pend = 0;
+        s.obs_limit = jt;
+        s.tail_src = (!s.crossing && s.t >= tf - eps_t) ? SRC_Y : -1;
+        refill(s, P);
+        int after;
+        if (s.crossing) after = JUMP;
+        else if (s.tail_src >= 0 || s.grid >= P.n_t) after = FINISH;
+        else after = RUN;
+        s.after_obs = after;
+        s.next_phase = has_more(s, P) ? OBS : after;
+      }
+      __syncthreads();
+    }
+
+    // ---------------- round end: outputs of finishing slots, phase advance ----------------
+    if (threadIdx.x < B) {
+      Slot& s = S[threadIdx.x];
+      if (s.phase == FINISH) {  // its last observations were taken in this round's P1
+        P.status[s.sys] = s.status == kRunning ? kDone : s.status;
+        P.fail_t[s.sys] = s.t;
+        P.stats[s.sys * 3] = s.steps;
+        P.stats[s.sys * 3 + 1] = s.rejected;
+        P.stats[s.sys * 3 + 2] = s.rhs_evals;
+        P.jump_count[s.sys] = s.njumps;
+        s.next_phase = FREE;
+      } else if (s.phase == OBS) {
+        refill(s, P);
+        s.next_phase = s.n_pend > 0 ? OBS : s.after_obs;
+      }
+      if (s.phase != DONE) s.phase = s.next_phase;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+int batch_slots() { return B; }
+
+size_t batch_work_stride(int n) { return static_cast<size_t>(NBUF) * static_cast<size_t>(n) * B; }
+
+int batch_max_blocks_per_sm() {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, batch_kernel, kThreads, 0);
+  return nb;
+}
+
+cudaError_t launch_batch(const BatchProblem& P, int grid, cudaStream_t s) {
+  batch_kernel<<<grid, kThreads, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace qsg

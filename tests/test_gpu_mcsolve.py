@@ -1,0 +1,127 @@
+"""GPU parity of the batched Monte-Carlo engine (qsg_mcsolve) and the parameter-sweep engine
+(qsg_mesolve_batch) against the CPU oracle, plus the reference's statistical assertions.
+
+Per-trajectory parity: trajectory i draws from RngStream(seed, i) on both sides, so jump
+channels must agree exactly and jump times / observables within the integrator tolerance.
+"""
+import numpy as np
+import pytest
+
+import paper_2504_21440_b200 as q
+from oracle import oracle as O
+from tests._helpers import assert_stats_close, csr_from_oracle, e_ops_csr, normwise_rel, oracle_generator
+
+pytestmark = pytest.mark.gpu
+
+
+def _mc(ctx, m, tlist, seed, b, e, **kw):
+    gen = oracle_generator(ctx, m, "mc")
+    cops = [csr_from_oracle(m, O.C_OP, k) for k in range(m.n_cops)]
+    return q.mcsolve(ctx, gen, cops, e_ops_csr(m), m.dim, m.psi0(), tlist, seed, b, e, **kw)
+
+
+def _compare_trajectories(dev, ref, lo=0, jt_tol=1e-6, ex_tol=1e-6, allow_diverged=0):
+    diverged = 0
+    for i in range(min(len(dev["jumps"]), len(ref["jumps"]) - lo)):
+        dj, rj = dev["jumps"][i], ref["jumps"][lo + i]
+        same = len(dj) == len(rj) and all(a[1] == b[1] and abs(a[0] - b[0]) <= jt_tol * max(1, abs(b[0]))
+                                          for a, b in zip(dj, rj))
+        if not same:
+            diverged += 1
+            continue
+        assert normwise_rel(dev["per_traj"][i], ref["per_traj"][lo + i]) <= ex_tol, i
+    assert diverged <= allow_diverged, diverged
+
+
+def test_mc_threshold_crossing_located(ctx):
+    """test_trajectories.cpp:66-88 on the device: |exp(-g t_jump) - r| < 5e-10."""
+    m = O.Model("decay2", 0.8)
+    r = _mc(ctx, m, np.linspace(0, 30, 31), 99, 0, 64, abstol=1e-13, reltol=1e-12)
+    assert r["n_ok"] == 64
+    for i in range(64):
+        assert len(r["jumps"][i]) == 1
+        u = O.rng(99, i, 2, 1)[0]
+        assert abs(np.exp(-0.8 * r["jumps"][i][0][0]) - u) < 5e-10
+
+
+def test_mc_decay_law_and_oracle_parity(ctx):
+    """test_trajectories.cpp:40-64 statistics + per-trajectory parity with the oracle."""
+    m = O.Model("decay2", 0.25)
+    t = np.linspace(0, 80, 41)
+    dev = _mc(ctx, m, t, 2025, 0, 2000)
+    times = np.array([j[0][0] for j in dev["jumps"]])
+    assert all(len(j) == 1 for j in dev["jumps"])
+    assert abs(times.mean() - 4.0) / 4.0 < 0.05
+    ref = m.mcsolve(t, 2025, 256)
+    _compare_trajectories(dev, ref)
+
+
+def test_mc_jc_per_trajectory_parity(ctx):
+    m = O.Model("jc", 6, 1.0, 1.0, 0.1, 0.05, 0.05)
+    t = np.linspace(0, 60, 61)
+    dev = _mc(ctx, m, t, 7, 0, 16)
+    ref = m.mcsolve(t, 7, 16)
+    _compare_trajectories(dev, ref)
+    for i in range(16):
+        assert_stats_close(dev["stats"][i], ref["stats"][i], restarts=len(ref["jumps"][i]))
+
+
+def test_mc_ising_trajectory_block_independent(ctx):
+    """Any partition of the trajectory range gives identical per-trajectory results."""
+    m = O.Model("ising", 6, 1, 1.0, 0.2, 1.0, 1)
+    t = np.linspace(0, 10, 100)
+    full = _mc(ctx, m, t, 2025, 0, 24)
+    part = _mc(ctx, m, t, 2025, 8, 16)
+    assert part["jumps"] == full["jumps"][8:16]
+    assert np.array_equal(part["per_traj"], full["per_traj"][8:16])
+    ref = m.mcsolve(t, 2025, 24)
+    _compare_trajectories(full, ref, allow_diverged=1)
+
+
+def test_mc_mean_matches_mesolve_4sigma(ctx):
+    """test_trajectories.cpp:90-114: |mc - me| <= 4 sigma/sqrt(N) + 1e-3 at every grid point."""
+    m = O.Model("jc", 10, 1.0, 1.0, 0.1, 0.01, 0.01)
+    t = np.linspace(0, 10 * np.pi / 0.1, 101)
+    n = 400
+    dev = _mc(ctx, m, t, 7, 0, n)
+    me, _, _ = m.mesolve(t)
+    mean = dev["block_sum"] / dev["n_ok"]
+    sd = np.std(dev["per_traj"][:, 0, :].real, axis=0, ddof=1)
+    assert np.all(np.abs(mean[0].real - me[0].real) <= 4 * sd / np.sqrt(n) + 1e-3)
+
+
+def test_mc_zero_collapse_reduces_to_sesolve(ctx):
+    m = O.Model("jc", 8, 1.0, 1.0, 0.1, 0.0, 0.0)
+    t = np.linspace(0, 25, 26)
+    dev = _mc(ctx, m, t, 5, 0, 3, abstol=1e-12, reltol=1e-11)
+    se, _, _ = m.sesolve(t, abstol=1e-12, reltol=1e-11)
+    assert all(len(j) == 0 for j in dev["jumps"])
+    assert np.max(np.abs(dev["block_sum"] / 3 - se)) < 1e-9
+
+
+def test_ensemble_combine_matches_pairwise(ctx):
+    """Blocks [0,5000) [5000,10000)-style tiling reproduces the single-block bracket bitwise."""
+    m = O.Model("jc", 6, 1.0, 1.0, 0.1, 0.05, 0.05)
+    t = np.linspace(0, 20, 21)
+    full = _mc(ctx, m, t, 11, 0, 64)
+    blocks = [(0, 16), (16, 32), (32, 48), (48, 64)]
+    parts = [_mc(ctx, m, t, 11, b, e) for b, e in blocks]
+    mean = q.ensemble_combine(blocks, [p["block_sum"] for p in parts], 64)
+    ref = full["block_sum"] / 64
+    assert np.array_equal(mean.view(np.float64), ref.view(np.float64))
+
+
+def test_mesolve_batch_sweep_parity(ctx):
+    """Parameter sweep (a14): per-point device results vs one oracle mesolve per point."""
+    m = O.Model("coupled_kerr", 4, 0.1, 0.5, 1.0)
+    gen = oracle_generator(ctx, m, "me")
+    t = np.linspace(0, 10, 101)
+    pts = np.array([[d, f] for d in (-2.0, 0.0, 1.3) for f in (0.1, 0.55, 1.0)])
+    rho0 = np.zeros(m.dim * m.dim, complex)
+    rho0[0] = 1.0
+    res = q.mesolve_batch(ctx, gen, m.dim, rho0, t, e_ops_csr(m), pts)
+    assert np.all(res["status"] == 0)
+    for p, prm in enumerate(pts):
+        ex, st, _ = m.mesolve(t, params=prm)
+        assert normwise_rel(res["expect"][p], ex) <= 1e-6, p
+        assert_stats_close(res["stats"][p], st)
