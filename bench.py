@@ -1,0 +1,379 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 time-evolution hot path (BASELINE.json configs).
+
+Headline (N = 1, BASELINE configs[1]): mesolve of the dissipative transverse-field Ising chain,
+10 spins (Liouvillian 4^10 = 1,048,576 rows, 24.6 M entries), Dormand-Prince 5(4) with the
+reference defaults abstol 1e-8 / reltol 1e-6, tlist = linspace(0, 10, 100), e_ops Sx/Sy/Sz
+totals. One "step" = one complete solve. `value` = device time per solve with the operator,
+initial state and e_ops resident in HBM; `e2e` = the same solve through the C-ABI with host
+buffers (operator store upload from pinned host CSR + rho0 in, expectations out).
+
+For N > 1 (torchrun, one process per GPU) mesolve runs as independent replicas (a single solve
+does not shard); the sharded workload — mcsolve trajectories of the 14-spin chain
+combined with an NCCL all-gather of the per-rank pairwise block sums — is reported under
+`secondary.mcsolve` at every N.
+
+`--impl reference` times the CPU restatement of the reference (oracle/, single-threaded as the
+reference's mesolve) on a bounded sample of the same workload (the first 0.5 time units),
+extrapolated per DP5 attempt to the full solve.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+TLIST = np.linspace(0.0, 10.0, 100)
+TFIM = (10, 1, 1.0, 0.2, 1.0, 1)       # nx, ny, Jz, hx, gamma, periodic (scenarios/ising_mc_2x3.json:5)
+TFIM_MC = (14, 1, 1.0, 0.2, 1.0, 1)
+MC_SEED = 2025
+
+
+def hbm_peak():
+    try:
+        with open(MEASURED) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+                for i, nm in enumerate(names):
+                    if f[4 + i].lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def csr_bytes(m):
+    return m.rowptr.nbytes + m.col.nbytes + m.val.nbytes
+
+
+# ---------------------------------------------------------------------------------------------------
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2504_21440_b200 as q
+
+    dev = local
+    torch.cuda.set_device(dev)
+    ctx = q.Context(dev)
+    peak, peak_src = hbm_peak()
+
+    # ---- host model assembly with the product's C++ API (timed separately, not part of value)
+    t0 = time.perf_counter()
+    model = q.Model("ising", *TFIM)
+    L = model.export(q.SEL_L_CONST)
+    eops = [model.export(q.SEL_E_OP, k) for k in range(model.n_eops)]
+    host_build_s = time.perf_counter() - t0
+    d, n, nnz = model.dim, L.n_rows, L.nnz
+    psi = model.psi0()
+    rho0 = np.outer(psi, psi.conj()).reshape(-1, order="F").copy()
+
+    t0 = time.perf_counter()
+    op = ctx.op(L)
+    store_build_s = time.perf_counter() - t0
+    gen = q.Generator([op])
+    rho0_dev = torch.from_numpy(rho0).to(f"cuda:{dev}")
+
+    # ---- warm-up, then K timed solves (device-timed persistent kernel, max over ranks)
+    for _ in range(args.warmup):
+        r = q.mesolve(ctx, gen, d, rho0_dev, TLIST, eops)
+    barrier(ws)
+    torch.cuda.synchronize()
+    kms, attempts = [], []
+    with ClockSampler(dev) as clk:
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            r = q.mesolve(ctx, gen, d, rho0_dev, TLIST, eops)
+            kms.append(r["kernel_ms"])
+            attempts.append(r["attempts"])
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    barrier(ws)
+    ms_step = allreduce_max(sum(kms) / len(kms), ws)
+    value_s = ms_step / 1e3
+    att = attempts[-1]
+    stats = r["stats"]
+
+    # ---- roofline of the fused DP5 kernel (SURVEY.md §8d byte model, per launch = per solve)
+    b_att = 6 * (20 * nnz + 4 * (n + 1)) + 47 * 16 * n
+    b_init = 2 * (20 * nnz + 4 * (n + 1)) + 6 * 16 * n
+    alg_bytes = b_att * att + b_init
+    achieved = alg_bytes / (ms_step / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "dp5_grid_kernel_dram_bytes.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the C-ABI with host buffers (pinned), copies inside the timed region
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
+    Lh = q.CsrMatrix(pin(L.rowptr), pin(L.col), pin(L.val), L.n_rows, L.n_cols)
+    rho0_h = pin(rho0)
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        op2 = ctx.op(Lh)
+        r2 = q.mesolve(ctx, q.Generator([op2]), d, rho0_h, TLIST, eops)
+        _ = r2["expect"].sum()
+        op2.close()
+    e2e_s = allreduce_max((time.perf_counter() - t0) / e2e_steps, ws)
+    h2d = csr_bytes(L) + rho0.nbytes + sum(csr_bytes(e) for e in eops)
+    d2h = r2["expect"].nbytes
+
+    # ---- secondary: plain SpMV of the operator store (SpMV HBM GB/s metric)
+    y = torch.randn(n, dtype=torch.complex128, device=f"cuda:{dev}")
+    out = torch.empty_like(y)
+    spmv_ms = q.generator_apply_timed(ctx, gen, y, out, reps=20)
+    spmv_bytes = 20 * nnz + 4 * (n + 1) + 32 * n
+    secondary = {"spmv_tfim10": {"ms": spmv_ms, "GBps": spmv_bytes / spmv_ms / 1e6,
+                                 "frac": spmv_bytes / spmv_ms / 1e6 / peak, "bytes_model": "20*nnz+4*(n+1)+32*n"}}
+    if not args.quick:
+        secondary["kerr_sweep_spmv"] = kerr_sweep_spmv(ctx, q, torch, dev, peak)
+        secondary["mcsolve"] = mcsolve_sharded(args, ctx, q, torch, ws, rank)
+    del out, y
+
+    line = {
+        "metric": "mesolve_time_to_solution",
+        "value": value_s,
+        "unit": "s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128",
+        "data": "synthetic: reference TFIM construction (factories.cpp:204-246), all-up initial state",
+        "config": {
+            "workload": "mesolve dissipative TFIM chain, 10 spins, periodic (BASELINE configs[1])",
+            "liouvillian_rows": n, "liouvillian_nnz": nnz, "tlist": "linspace(0,10,100)",
+            "abstol": 1e-8, "reltol": 1e-6, "e_ops": "Sx,Sy,Sz totals", "method": "Dormand-Prince 5(4)",
+            "parallelism": f"replicas x{ws}" if ws > 1 else "single solve, one cooperative grid",
+            "l2_flush": "inputs exceed L2 (operator 497 MB > 126 MB L2)",
+            "dp5_attempts": att, "stats_steps_rejected_rhs": list(stats),
+            "host_build_s": host_build_s, "operator_store_build_s": store_build_s,
+            "grid_ctas": r["grid_ctas"], "timed_wall_s": wall,
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "dp5_grid_kernel (persistent fused DP5 solve, 1 launch per solve)",
+                     "bytes_model": "per attempt 6*(20*nnz+4*(n+1)) + 47*16*n (SURVEY.md 8d) + start 2 SpMV"},
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "path": "qsg_op_create(pinned host CSR) + qsg_mesolve(host rho0 -> host expect)"},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "secondary": secondary,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(att)
+    ctx.close()
+    return line
+
+
+def kerr_sweep_spmv(ctx, q, torch, dev, peak):
+    """BASELINE configs[3]: Liouvillian SpMV of the Kerr resonator for N = 50..400 (L2-resident
+    for the smaller cutoffs, so bytes/time can exceed the HBM copy rate)."""
+    out = {}
+    for N in (50, 100, 200, 400):
+        m = q.Model("kerr", N, 1.0, 0.01, 2.0, 1.0)
+        Lk = m.export(q.SEL_L_CONST)
+        g = q.Generator([ctx.op(Lk)])
+        y = torch.randn(Lk.n_rows, dtype=torch.complex128, device=f"cuda:{dev}")
+        o = torch.empty_like(y)
+        ms = q.generator_apply_timed(ctx, g, y, o, reps=50)
+        b = 20 * Lk.nnz + 4 * (Lk.n_rows + 1) + 32 * Lk.n_rows
+        out[f"N{N}"] = {"rows": Lk.n_rows, "nnz": Lk.nnz, "us": ms * 1e3, "GBps": b / ms / 1e6}
+    return out
+
+
+def mcsolve_sharded(args, ctx, q, torch, ws, rank):
+    """BASELINE configs[2] workload (TFIM-14 mcsolve) on a bounded trajectory count, sharded in
+    contiguous blocks (trajectory i = RngStream(2025, i) on every N), NCCL all-gather of block sums."""
+    ntraj = args.mc_traj
+    m = q.Model("ising", *TFIM_MC)
+    G = q.Generator([ctx.op(m.export(q.SEL_MC_GEN))])
+    cops = [m.export(q.SEL_C_OP, k) for k in range(m.n_cops)]
+    eops = [m.export(q.SEL_E_OP, 2)]
+    b, e = ntraj * rank // ws, ntraj * (rank + 1) // ws
+    barrier(ws)
+    r = q.mcsolve(ctx, G, cops, eops, m.dim, m.psi0(), TLIST, MC_SEED, b, e, per_traj=False)
+    t_ms = allreduce_max(r["kernel_ms"], ws)
+    bs = r["block_sum"]
+    if ws > 1:
+        import torch.distributed as dist
+        mine = torch.from_numpy(np.concatenate([bs.reshape(-1), [r["n_ok"]]]).astype(np.complex128)).cuda()
+        gathered = [torch.empty_like(mine) for _ in range(ws)]
+        dist.all_gather(gathered, mine)
+        parts = [g.cpu().numpy() for g in gathered]
+        sums = [p[:-1].reshape(bs.shape) for p in parts]
+        n_ok = int(sum(p[-1].real for p in parts))
+        ranges = [(ntraj * k // ws, ntraj * (k + 1) // ws) for k in range(ws)]
+        mean = q.ensemble_combine(ranges, sums, n_ok)
+    else:
+        n_ok = r["n_ok"]
+        mean = bs / n_ok
+    return {"workload": "mcsolve TFIM-14 (16384-dim), Sz_total, tlist linspace(0,10,100)",
+            "ntraj": ntraj, "n_ok": n_ok, "device_s": t_ms / 1e3, "traj_per_s": ntraj / (t_ms / 1e3),
+            "attempts_rank0": r["attempts"], "mean_Sz_t10": float(mean[0, -1].real),
+            "collective": "torch.distributed all_gather (NCCL) of per-rank pairwise block sums" if ws > 1 else None}
+
+
+def cpu_baseline(gpu_attempts):
+    """Oracle (CPU restatement of the reference solve loop) on the first 0.5 time units of the
+    same solve with a prebuilt Liouvillian; per-attempt time extrapolated to the full solve."""
+    from oracle import oracle as O
+    m = O.Model("ising", *TFIM)
+    t0 = time.perf_counter()
+    m.prepare_liouvillian()
+    build = time.perf_counter() - t0
+    sample_t = np.linspace(0.0, 0.5, 6)
+    t0 = time.perf_counter()
+    _, st = m.mesolve_prepared(sample_t)
+    dt = time.perf_counter() - t0
+    per_att = dt / int(st[0] + st[1])
+    return {"value": per_att * gpu_attempts, "unit": "s", "cores": 1, "kind": "port",
+            "sample": f"oracle mesolve TFIM-10 over t in [0,0.5] ({int(st[0] + st[1])} DP5 attempts, "
+                      f"{dt:.1f} s), {per_att:.3f} s/attempt x {gpu_attempts} attempts of the full solve; "
+                      f"Liouvillian build {build:.1f} s excluded"}
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the CPU restatement of the reference on this host (rank 0 only)."""
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+    m = O.Model("ising", *TFIM)
+    t0 = time.perf_counter()
+    m.prepare_liouvillian()
+    build = time.perf_counter() - t0
+    sample_t = np.linspace(0.0, 0.5, 6)
+    full_attempts = 81  # DP5 attempts of the full TFIM-10 solve (device and oracle agree: 80 + 1)
+    for _ in range(args.warmup if args.warmup <= 1 else 1):
+        m.mesolve_prepared(sample_t)
+    vals = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, st = m.mesolve_prepared(sample_t)
+        dt = time.perf_counter() - t0
+        vals.append(dt / int(st[0] + st[1]) * full_attempts)
+    v = sum(vals) / len(vals)
+    sample = (f"oracle (CPU restatement of evolve.cpp/integrator.hpp) TFIM-10 over t in [0,0.5] per step, "
+              f"per-attempt time x {full_attempts} attempts; 1 thread (reference mesolve is single-threaded, "
+              f"SPEC.md:382); Liouvillian build {build:.1f} s excluded")
+    return {"metric": "mesolve_time_to_solution", "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic: reference TFIM construction",
+            "config": {"workload": "mesolve dissipative TFIM chain, 10 spins, periodic (BASELINE configs[1])"},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mc-traj", type=int, default=2368)
+    ap.add_argument("--quick", action="store_true", help="headline only (no secondary workloads)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        line = run_reference(args, ws, rank)
+    else:
+        line = run_ours(args, ws, rank, local)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

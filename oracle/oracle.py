@@ -53,6 +53,8 @@ def lib():
         L.orc_splitmix64.restype = C.c_ulonglong
         L.orc_splitmix64.argtypes = [C.POINTER(C.c_ulonglong)]
         L.orc_ising_capped.argtypes = [C.c_int, C.c_int]
+        L.orc_model_prepare_liouvillian.argtypes = [P]
+        L.orc_mesolve_prepared.argtypes = [P, DP, C.c_int, DP, C.c_int, DP, DP, LP]
         _lib = L
     return _lib
 
@@ -153,6 +155,20 @@ class Model:
     def sesolve(self, tlist, params=None, abstol=1e-8, reltol=1e-6, max_steps=10_000_000,
                 store_states=False, saveat=None):
         return self._solve("se", tlist, params, abstol, reltol, max_steps, store_states, saveat)
+
+    def prepare_liouvillian(self):
+        """Build L once (the reference's liouvillian()); timed separately from the solve."""
+        _check(lib().orc_model_prepare_liouvillian(self._h))
+
+    def mesolve_prepared(self, tlist, params=None, abstol=1e-8, reltol=1e-6, max_steps=10_000_000):
+        t = np.ascontiguousarray(tlist, np.float64)
+        prm = np.ascontiguousarray(self.default_params if params is None else params, np.float64)
+        opts = self._opts(abstol, reltol, max_steps, False)
+        expect = np.zeros(self.n_eops * len(t), np.complex128)
+        stats = np.zeros(3, np.int64)
+        _check(lib().orc_mesolve_prepared(self._h, _dp(t), len(t), _dp(prm), len(prm), _dp(opts),
+                                          expect.ctypes.data_as(DP), stats.ctypes.data_as(LP)))
+        return expect.reshape(len(t), self.n_eops).T.copy(), stats
 
     def mcsolve(self, tlist, seed, ntraj, n_threads=0, params=None, abstol=1e-8, reltol=1e-6,
                 max_steps=10_000_000, jcap=512):

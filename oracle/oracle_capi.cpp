@@ -13,6 +13,7 @@ thread_local std::string g_err;
 
 struct Handle {
   Model m;
+  std::unique_ptr<TdOp> L;  // prebuilt Liouvillian (SuperOperator input path, evolve.cpp:244-252)
 };
 
 int fail(const std::exception& e) {
@@ -169,6 +170,38 @@ int orc_sesolve(void* hp, const double* tlist, int nt, const double* params, int
         off += d.v.size();
       }
     }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+/// Build and cache L = liouvillian(H, c_ops) (td terms kept) for orc_mesolve_prepared.
+int orc_model_prepare_liouvillian(void* hp) {
+  try {
+    auto* h = static_cast<Handle*>(hp);
+    h->L = std::make_unique<TdOp>(liouvillian_td(h->m.h, h->m.c_ops));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+/// mesolve on the cached SuperOperator (c_ops empty), i.e. the reference's solve loop without the
+/// Liouvillian assembly — what the CPU baseline times.
+int orc_mesolve_prepared(void* hp, const double* tlist, int nt, const double* params, int np,
+                         const double* opts, double* expect, long* stats) {
+  try {
+    auto* h = static_cast<Handle*>(hp);
+    if (!h->L) throw_error(ErrorCode::InvalidGrid, "call orc_model_prepare_liouvillian first");
+    const Model& m = h->m;
+    Params prm = np > 0 ? Params(params, params + np) : m.params;
+    SolveResult r = mesolve(*h->L, m.psi0, std::span<const double>(tlist, static_cast<size_t>(nt)), {},
+                            m.e_ops, prm, to_opts(opts, 0, nullptr));
+    write_dense(r.expect, expect);
+    stats[0] = r.stats.steps;
+    stats[1] = r.stats.rejected;
+    stats[2] = r.stats.rhs_evals;
     return 0;
   } catch (const std::exception& e) {
     return fail(e);
