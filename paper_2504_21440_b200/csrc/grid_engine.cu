@@ -1,16 +1,19 @@
 // Persistent cooperative Dormand-Prince 5(4) solver for ONE large system (mesolve / sesolve).
 //
 // One launch integrates the whole tlist: every CTA of a cooperative grid owns a contiguous
-// slab of 32-row blocks; the six RHS evaluations of an attempt (integrator.hpp:91-102) are
-// fused CSR SpMV passes whose epilogue forms the next stage input, the stage-7 pass also
-// produces the embedded-error partials (integrator.hpp:105-116), and the accept/reject PI
-// controller (integrator.hpp:119-145) runs redundantly — and identically — in every CTA after
-// a deterministic grid reduction. Observations (evolve.cpp:160-165, 284-297) evaluate the
-// Hairer dense output (integrator.hpp:127-131,150-154) lazily, only at the indices the e_ops
-// touch, fused into the next attempt's first pass. No host round trip per step.
+// range of 32-row SELL slices; the six RHS evaluations of an attempt (integrator.hpp:91-102) are
+// fused SpMV passes whose epilogue forms the next stage input, the stage-7 pass also produces
+// the embedded-error partials (integrator.hpp:105-116), and the accept/reject PI controller
+// (integrator.hpp:119-145) runs redundantly — and identically — in every CTA after a
+// deterministic grid reduction. Observations (evolve.cpp:160-165, 284-297) evaluate the Hairer
+// dense output (integrator.hpp:127-131,150-154) lazily, only at the indices the e_ops touch,
+// fused into the next attempt's first pass. No host round trip per step.
 //
-// Passes per attempt: 6 (stage 2 gathers y + h*a21*k1 on the fly), each followed by one grid
-// barrier. See DESIGN.md §4 for the byte model.
+// Register budget: the integrator state lives in shared memory and is advanced by thread 0 of
+// each CTA between barriers; the SpMV passes only hold the buffer pointers they touch, which
+// keeps the kernel at <= 64 registers and 2 CTAs x 16 warps per SM for latency hiding.
+//
+// Passes per attempt: 6 (stage 2 gathers y + h*a21*k1 on the fly), one grid barrier each.
 #include <cstdio>
 
 #include "engine.cuh"
@@ -21,6 +24,9 @@ namespace qsg {
 namespace {
 
 constexpr int kThreads = 512;
+#ifndef QSG_GRID_MINB
+#define QSG_GRID_MINB 2
+#endif
 
 struct Pending {
   double theta;  // NaN: observe buffer Y directly
@@ -28,29 +34,33 @@ struct Pending {
   int save_idx;  // -1: no state save
 };
 
-struct Bufs {
-  double2* b[11];
-};
-
 // logical buffer ids
 enum { Y = 0, YO = 1, K1 = 2, K2 = 3, K3 = 4, K4 = 5, K5 = 6, K6 = 7, K7 = 8, SA = 9, SB = 10 };
 
-__device__ __forceinline__ double2 dense_at(double2* const* B, const int* bi, int c, double theta,
-                                            double h) {
-  // integrator.hpp:127-131 (rc1..rc5) and :150-154 (evaluation), per element.
-  // After an accepted step the FSAL swap (:138) put the step's k1 under the K7 label and its
-  // k7 under the K1 label.
-  const double2 yo = B[bi[YO]][c];
-  if (isnan(theta)) return B[bi[Y]][c];
-  const double2 y1 = B[bi[Y]][c];
-  const double2 k1 = B[bi[K7]][c];
-  const double2 k7 = B[bi[K1]][c];
-  const double2 k3 = B[bi[K3]][c], k4 = B[bi[K4]][c], k5 = B[bi[K5]][c], k6 = B[bi[K6]][c];
+// Integrator state of the solve — identical in every CTA, written by thread 0 only.
+struct Ctl {
+  double2* p[11];  // logical -> physical buffer (FSAL / y rotation, integrator.hpp:133-138)
+  double t, t_old, h, h_last, facold, hh, h0, d1;
+  double fail_t;
+  long long steps, rejected, rhs_evals, attempts_total;
+  int status, clamped, attempts, next, np, obs_par, flush, done;
+  Pending pend[kMaxPending];
+};
+
+__device__ __forceinline__ double2 dense_at(double2* const* p, int c, double theta, double h) {
+  // integrator.hpp:127-131 (rc1..rc5) and :150-154 (evaluation), per element. After an accepted
+  // step the FSAL swap (:138) put the step's k1 under the K7 label and its k7 under K1.
+  if (isnan(theta)) return p[Y][c];
+  const double2 yo = p[YO][c];
+  const double2 y1 = p[Y][c];
+  const double2 k1 = p[K7][c];
+  const double2 k7 = p[K1][c];
+  const double2 k3 = p[K3][c], k4 = p[K4][c], k5 = p[K5][c], k6 = p[K6][c];
   using namespace dp;
   const double th1 = 1.0 - theta;
-  double2 rc2 = csub(y1, yo);
-  double2 rc3 = csub(cscale(h, k1), rc2);
-  double2 rc4 = csub(csub(rc2, cscale(h, k7)), rc3);
+  const double2 rc2 = csub(y1, yo);
+  const double2 rc3 = csub(cscale(h, k1), rc2);
+  const double2 rc4 = csub(csub(rc2, cscale(h, k7)), rc3);
   double2 rc5;
   rc5.x = h * (d1 * k1.x + d3 * k3.x + d4 * k4.x + d5 * k5.x + d6 * k6.x + d7 * k7.x);
   rc5.y = h * (d1 * k1.y + d3 * k3.y + d4 * k4.y + d5 * k5.y + d6 * k6.y + d7 * k7.y);
@@ -60,38 +70,39 @@ __device__ __forceinline__ double2 dense_at(double2* const* B, const int* bi, in
   return o;
 }
 
-// Observation pass for up to `np` pending events: expectation partials into reduction slots
-// and state saves. ME: expect_e = sum_{(i,j) in A_e} A(i,j) * rho_h(j,i) with
-// rho_h = (rho + rho^dag)/2 (evolve.cpp:286-295); SE: <psi|E psi> (evolve.cpp:341-345).
+// Observation pass for the pending events: expectation partials into reduction slots and state
+// saves. ME: expect_e = sum_{(i,j) in A_e} A(i,j) * rho_h(j,i), rho_h = (rho + rho^dag)/2
+// (evolve.cpp:286-295); SE: <psi|E psi> (evolve.cpp:341-345).
 template <int MODE>
-__device__ void observe_pass(const GridProblem& P, double2* const* B, const int* bi,
-                             const Pending* pend, int np, double h_last, double* slots,
-                             double* smem, int rank, int G) {
+__device__ __noinline__ void observe_pass(const GridProblem& P, const Ctl& c, double* slots, double* smem,
+                                          int rank, int G) {
+  double2* const* p = c.p;
+  const int np = c.np;
+  const double h_last = c.h_last;
   const int gtid = rank * blockDim.x + threadIdx.x;
   const int gstride = G * blockDim.x;
   for (int e = 0; e < P.n_e; ++e) {
     for (int q = 0; q < np; ++q) {
       double2 acc = make_double2(0.0, 0.0);
-      if (pend[q].grid_idx >= 0) {
+      const double th = c.pend[q].theta;
+      if (c.pend[q].grid_idx >= 0) {
         if (MODE == 0) {
           const int beg = P.eo_off[e], end = P.eo_off[e + 1];
-          for (int p = beg + gtid; p < end; p += gstride) {
-            const int i = P.eo_i[p], j = P.eo_j[p];
-            // rho(j,i) = y[i*d + j], rho(i,j) = y[j*d + i]
-            const double2 rji = dense_at(B, bi, i * P.d + j, pend[q].theta, h_last);
-            const double2 rij = dense_at(B, bi, j * P.d + i, pend[q].theta, h_last);
+          for (int k = beg + gtid; k < end; k += gstride) {
+            const int i = P.eo_i[k], j = P.eo_j[k];
+            const double2 rji = dense_at(p, i * P.d + j, th, h_last);  // rho(j,i) = y[i*d + j]
+            const double2 rij = dense_at(p, j * P.d + i, th, h_last);  // rho(i,j) = y[j*d + i]
             const double2 rh = cscale(0.5, cadd(rji, cconj(rij)));
-            acc = cadd(acc, cmul(P.eo_v[p], rh));
+            acc = cadd(acc, cmul(P.eo_v[k], rh));
           }
         } else {
           const int* rp = P.se_rowptr + static_cast<long long>(e) * (P.n + 1);
           const long long off = P.se_off[e];
           for (int r = gtid; r < P.n; r += gstride) {
             double2 ev = make_double2(0.0, 0.0);
-            for (int p = rp[r]; p < rp[r + 1]; ++p)
-              ev = cadd(ev, cmul(P.se_val[off + p], dense_at(B, bi, P.se_col[off + p], pend[q].theta, h_last)));
-            const double2 g = dense_at(B, bi, r, pend[q].theta, h_last);
-            acc = cadd(acc, cmul(cconj(g), ev));
+            for (int k = rp[r]; k < rp[r + 1]; ++k)
+              ev = cadd(ev, cmul(P.se_val[off + k], dense_at(p, P.se_col[off + k], th, h_last)));
+            acc = cadd(acc, cmul(cconj(dense_at(p, r, th, h_last)), ev));
           }
         }
       }
@@ -104,391 +115,390 @@ __device__ void observe_pass(const GridProblem& P, double2* const* B, const int*
       }
     }
   }
-  // state saves: every CTA writes its own rows
-  for (int q = 0; q < np; ++q) {
-    if (pend[q].save_idx < 0) continue;
-    double2* out = P.states + static_cast<long long>(pend[q].save_idx) * P.n;
+  for (int q = 0; q < np; ++q) {  // state saves: every CTA writes its share
+    if (c.pend[q].save_idx < 0) continue;
+    const double th = c.pend[q].theta;
+    double2* out = P.states + static_cast<long long>(c.pend[q].save_idx) * P.n;
     for (int r = gtid; r < P.n; r += gstride) {
       if (MODE == 0) {
         const int i = r % P.d, j = r / P.d;
-        const double2 a = dense_at(B, bi, r, pend[q].theta, h_last);          // rho(i,j)
-        const double2 b = dense_at(B, bi, i * P.d + j, pend[q].theta, h_last);  // rho(j,i)
+        const double2 a = dense_at(p, r, th, h_last);          // rho(i,j)
+        const double2 b = dense_at(p, i * P.d + j, th, h_last);  // rho(j,i)
         out[r] = cscale(0.5, cadd(a, cconj(b)));
       } else {
-        out[r] = dense_at(B, bi, r, pend[q].theta, h_last);
+        out[r] = dense_at(p, r, th, h_last);
       }
     }
   }
 }
 
 // CTA 0 folds the observation slots (written before the last barrier) into expect[].
-__device__ void observe_commit(const GridProblem& P, const Pending* pend, int np,
-                               const double* slots, int G) {
+__device__ __noinline__ void observe_commit(const GridProblem& P, const Ctl& c, const double* slots, int G) {
   if (blockIdx.x != 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int nv = 2 * np * P.n_e;
+  const int nv = 2 * c.np * P.n_e;
   for (int s = warp; s < nv; s += nw) {
     double v = 0.0;
     for (int g = lane; g < G; g += 32) v += slots[static_cast<long long>(s) * G + g];
     v = warp_sum(v);
     if (lane == 0) {
       const int q = (s / 2) / P.n_e, e = (s / 2) % P.n_e;
-      if (pend[q].grid_idx >= 0) {
-        double* dst = reinterpret_cast<double*>(P.expect + static_cast<long long>(pend[q].grid_idx) * P.n_e + e);
+      if (c.pend[q].grid_idx >= 0) {
+        double* dst = reinterpret_cast<double*>(P.expect + static_cast<long long>(c.pend[q].grid_idx) * P.n_e + e);
         dst[s & 1] = v;
       }
     }
   }
-  __syncthreads();  // s_pend is rewritten right after
 }
 
-// every CTA reads slot s (partials of all G CTAs) in the same order -> identical value
-__device__ __forceinline__ double grid_value(const double* red, int s, int G, double* smem) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (warp == 0) {
+// every CTA reads slot s (partials of all G CTAs) in the same order -> identical value in *out
+__device__ __forceinline__ void grid_value(const double* red, int s, int G, double* out) {
+  if ((threadIdx.x >> 5) == 0) {
+    const int lane = threadIdx.x & 31;
     double v = 0.0;
     for (int g = lane; g < G; g += 32) v += red[static_cast<long long>(s) * G + g];
     v = warp_sum(v);
-    if (lane == 0) smem[0] = v;
+    if (lane == 0) *out = v;
   }
-  __syncthreads();
-  return smem[0];
+}
+
+__device__ __forceinline__ void push_pending(const GridProblem& P, Ctl& c, double theta) {
+  c.pend[c.np] = Pending{theta, P.ev_grid[c.next], P.ev_save[c.next]};
+  ++c.np;
+  ++c.next;
+}
+
+// One fused stage pass: k_S = G(ts) x over this CTA's slices, then the stage epilogue
+// (integrator.hpp:91-102 for S = 2..6; error partial of :106-116 for S = 7).
+template <int S>
+__device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c, int s0, int s1) {
+  using namespace dp;
+  const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = P.n;
+  const double hh = c.hh;
+  const double ts = S == 2 ? c.t + c2 * hh : S == 3 ? c.t + c3 * hh : S == 4 ? c.t + c4 * hh
+                  : S == 5 ? c.t + c5 * hh : c.t + hh;
+  const double2* __restrict__ y = c.p[Y];
+  const double2* __restrict__ k1 = c.p[K1];
+  const double2* __restrict__ x = S == 2 ? nullptr : (S == 3 || S == 5 || S == 7) ? c.p[SA] : c.p[SB];
+  double esq = 0.0;
+  for (int b = s0 + warp; b < s1; b += W) {
+    const int row = (b << 5) + lane;
+    double2 k;
+    if (S == 2)
+      k = gen_row(P.gen, P.params, b, ts, [&](int col) {
+        const double2 a = y[col], q = k1[col];
+        return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
+      });
+    else
+      k = gen_row(P.gen, P.params, b, ts, [&](int col) { return x[col]; });
+    if (row >= n) continue;
+    const double2 yy = y[row], q1 = k1[row];
+    if (S == 2) {
+      c.p[K2][row] = k;
+      c.p[SA][row] = make_double2(yy.x + hh * (a31 * q1.x + a32 * k.x), yy.y + hh * (a31 * q1.y + a32 * k.y));
+    } else if (S == 3) {
+      const double2 q2 = c.p[K2][row];
+      c.p[K3][row] = k;
+      c.p[SB][row] = make_double2(yy.x + hh * (a41 * q1.x + a42 * q2.x + a43 * k.x),
+                                  yy.y + hh * (a41 * q1.y + a42 * q2.y + a43 * k.y));
+    } else if (S == 4) {
+      const double2 q2 = c.p[K2][row], q3 = c.p[K3][row];
+      c.p[K4][row] = k;
+      c.p[SA][row] = make_double2(yy.x + hh * (a51 * q1.x + a52 * q2.x + a53 * q3.x + a54 * k.x),
+                                  yy.y + hh * (a51 * q1.y + a52 * q2.y + a53 * q3.y + a54 * k.y));
+    } else if (S == 5) {
+      const double2 q2 = c.p[K2][row], q3 = c.p[K3][row], q4 = c.p[K4][row];
+      c.p[K5][row] = k;
+      c.p[SB][row] = make_double2(yy.x + hh * (a61 * q1.x + a62 * q2.x + a63 * q3.x + a64 * q4.x + a65 * k.x),
+                                  yy.y + hh * (a61 * q1.y + a62 * q2.y + a63 * q3.y + a64 * q4.y + a65 * k.y));
+    } else if (S == 6) {
+      const double2 q3 = c.p[K3][row], q4 = c.p[K4][row], q5 = c.p[K5][row];
+      c.p[K6][row] = k;
+      c.p[SA][row] = make_double2(yy.x + hh * (a71 * q1.x + a73 * q3.x + a74 * q4.x + a75 * q5.x + a76 * k.x),
+                                  yy.y + hh * (a71 * q1.y + a73 * q3.y + a74 * q4.y + a75 * q5.y + a76 * k.y));
+    } else {
+      const double2 y1 = x[row], q3 = c.p[K3][row], q4 = c.p[K4][row], q5 = c.p[K5][row], q6 = c.p[K6][row];
+      c.p[K7][row] = k;
+      double2 e;
+      e.x = hh * (e1 * q1.x + e3 * q3.x + e4 * q4.x + e5 * q5.x + e6 * q6.x + e7 * k.x);
+      e.y = hh * (e1 * q1.y + e3 * q3.y + e4 * q4.y + e5 * q5.y + e6 * q6.y + e7 * k.y);
+      const double sc = P.atol + P.rtol * fmax(cabs_(yy), cabs_(y1));
+      const double qq = cabs_(e) / sc;
+      esq += qq * qq;
+    }
+  }
+  return esq;
+}
+
+// start (integrator.hpp:61-69): k1 = G(t0) y and the d0/d1 norms of initial_step (:160-167)
+__device__ __noinline__ void start_pass(const GridProblem& P, const Ctl& c, int s0, int s1, double* d0,
+                                        double* d1) {
+  const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double2* y = c.p[Y];
+  double a0 = 0.0, a1 = 0.0;
+  for (int b = s0 + warp; b < s1; b += W) {
+    const int row = (b << 5) + lane;
+    const double2 k = gen_row(P.gen, P.params, b, c.t, [&](int col) { return y[col]; });
+    if (row < P.n) {
+      c.p[K1][row] = k;
+      const double2 yy = y[row];
+      const double sc = P.atol + P.rtol * cabs_(yy);
+      a0 += cnorm(make_double2(yy.x / sc, yy.y / sc));
+      a1 += cnorm(make_double2(k.x / sc, k.y / sc));
+    }
+  }
+  *d0 = a0;
+  *d1 = a1;
+}
+
+// initial_step trial evaluation (integrator.hpp:172-180): d2 partial of G(t0+h0)(y + h0 k1) - k1
+__device__ __noinline__ double start_pass2(const GridProblem& P, const Ctl& c, int s0, int s1) {
+  const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double2* y = c.p[Y];
+  const double2* k1 = c.p[K1];
+  const double h0 = c.h0;
+  double a = 0.0;
+  for (int b = s0 + warp; b < s1; b += W) {
+    const int row = (b << 5) + lane;
+    const double2 k = gen_row(P.gen, P.params, b, c.t + h0, [&](int col) {
+      const double2 u = y[col], v = k1[col];
+      return make_double2(u.x + h0 * v.x, u.y + h0 * v.y);
+    });
+    if (row < P.n) {
+      const double2 yy = y[row], kk1 = k1[row];
+      const double sc = P.atol + P.rtol * cabs_(yy);
+      const double2 df = csub(k, kk1);
+      a += cnorm(make_double2(df.x / sc, df.y / sc));
+    }
+  }
+  return a;
+}
+
+// thread 0: the Dopri5::step prologue for the next attempt (integrator.hpp:80-89) and the
+// max_steps guard of the solve loop (evolve.cpp:157-159).
+__device__ void begin_attempt(const GridProblem& P, Ctl& c) {
+  if (c.attempts == 0 && c.steps >= P.max_steps) {
+    c.status = kFailMaxSteps;
+    c.fail_t = c.t;
+    return;
+  }
+  c.hh = fmin(c.h, P.tf - c.t);
+  c.clamped = c.hh < c.h;
+  if (!(c.hh > 0.0)) {
+    c.status = kFailPastEnd;
+    c.fail_t = c.t;
+  } else if (c.hh <= fabs(c.t) * 1e-15 + 1e-300) {
+    c.status = kFailUnderflow;
+    c.fail_t = c.t;
+  } else if (++c.attempts > 1000) {
+    c.status = kFailRejected;
+    c.fail_t = c.t;
+  }
+}
+
+// thread 0: accept / reject (integrator.hpp:116-145) and event bookkeeping (evolve.cpp:160-165)
+__device__ void finish_attempt(const GridProblem& P, Ctl& c, double err_sq, int kcap) {
+  using namespace dp;
+  double err = sqrt(err_sq / static_cast<double>(P.n));
+  if (!isfinite(err)) err = 10.0;
+  c.rhs_evals += 6;
+  ++c.attempts_total;
+  if (err <= 1.0) {
+    const double fac11 = pow(err, expo1);
+    double fac = fac11 / pow(c.facold, beta);
+    fac = fmax(facc2, fmin(facc1, fac / safe));
+    const double h_new = c.hh / fac;
+    c.facold = fmax(err, 1e-4);
+    c.t_old = c.t;
+    c.t += c.hh;
+    c.h_last = c.hh;
+    double2* oy = c.p[Y];  // y_old <- y, y <- ysti7, FSAL k1 <-> k7
+    c.p[Y] = c.p[SA];
+    c.p[SA] = c.p[YO];
+    c.p[YO] = oy;
+    double2* k1p = c.p[K1];
+    c.p[K1] = c.p[K7];
+    c.p[K7] = k1p;
+    ++c.steps;
+    c.h = c.clamped ? fmax(c.h, h_new) : h_new;
+    c.attempts = 0;
+    while (c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t && c.np < kcap)
+      push_pending(P, c, (fmin(P.ev_t[c.next], c.t) - c.t_old) / c.h_last);
+    const bool more = c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t;
+    const bool last = c.t >= P.tf - P.eps_t;
+    c.flush = more || (last && c.np > 0);
+    c.done = last || c.next >= P.n_ev;
+  } else {
+    ++c.rejected;
+    c.h = c.hh / fmin(facc1, pow(err, expo1) / safe);
+    c.flush = 0;
+    c.done = 0;
+  }
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 1) dp5_grid_kernel(const __grid_constant__ GridProblem P) {
+__global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const __grid_constant__ GridProblem P) {
   __shared__ double s_red[kThreads / 32];
-  __shared__ double s_val;
-  __shared__ Pending s_pend[kMaxPending];
+  __shared__ double s_val[2];
+  __shared__ Ctl c;
 
   const int G = gridDim.x, rank = blockIdx.x;
-  const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = P.n;
-  const int nblk = (n + 31) >> 5;
-  const int bpc = (nblk + G - 1) / G;
-  const int b0 = rank * bpc, b1 = min(nblk, b0 + bpc);
-  double2* const* B = P.buf;
-  int bi[11];
-#pragma unroll
-  for (int i = 0; i < 11; ++i) bi[i] = i;
-
-  const double atol = P.atol, rtol = P.rtol;
-  const double t0 = P.t0, tf = P.tf, eps_t = P.eps_t;
+  const int nsl = (P.n + 31) >> 5;
+  const int spc = (nsl + G - 1) / G;
+  const int s0 = rank * spc, s1 = min(nsl, s0 + spc);
   double* red = P.red;
-  double* obs_slots[2] = {red + static_cast<long long>(kSlotObs0) * G,
-                          red + static_cast<long long>(kSlotObs0 + kObsSlots) * G};
-  int obs_par = 0;
-
-  double t = t0, t_old = t0, h = 0.0, h_last = 0.0, facold = 1e-4;
-  long long steps = 0, rejected = 0, rhs_evals = 0, attempts_total = 0;
-  int status = kRunning;
-  double fail_t = 0.0;
-  int next = 0, np = 0;
   const int kcap = max(1, min(kMaxPending, kObsSlots / (2 * max(1, P.n_e))));
-
-  auto push_pending = [&](double theta) {
-    // all threads run this identically; thread 0 also records it in shared memory
-    const int gi = P.ev_grid[next], si = P.ev_save[next];
-    if (threadIdx.x == 0) s_pend[np] = Pending{theta, gi, si};
-    ++np;
-    ++next;
+  auto slots = [&](int par) { return red + static_cast<long long>(kSlotObs0 + par * kObsSlots) * G; };
+  // observation flush: pass, barrier, CTA-0 commit (double-buffered slots)
+  auto flush_obs = [&]() {
+    observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
+    grid_barrier(P.bar, G);
+    observe_commit(P, c, slots(c.obs_par), G);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      c.obs_par ^= 1;
+      c.np = 0;
+    }
+    __syncthreads();
   };
 
-  // ---------------- start (integrator.hpp:61-69) + initial_step (:157-187) ----------------
-  // events at t0 observe y0 directly (evolve.cpp:134-137)
-  while (next < P.n_ev && P.ev_t[next] <= t0 + eps_t && np < kcap) push_pending(__longlong_as_double(0x7ff8000000000000ll));
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 11; ++i) c.p[i] = P.buf[i];
+    c.t = c.t_old = P.t0;
+    c.h = c.h_last = 0.0;
+    c.facold = 1e-4;
+    c.steps = c.rejected = c.rhs_evals = c.attempts_total = 0;
+    c.status = kRunning;
+    c.attempts = c.next = c.np = c.obs_par = c.flush = c.done = 0;
+    c.fail_t = 0.0;
+    // events at t0 observe y0 directly (evolve.cpp:134-137)
+    while (c.next < P.n_ev && P.ev_t[c.next] <= P.t0 + P.eps_t && c.np < kcap)
+      push_pending(P, c, __longlong_as_double(0x7ff8000000000000ll));
+  }
   __syncthreads();
+
+  // ---------------- start + initial_step ----------------
   {
-    // pass S1: k1 = G(t0) y ; d0, d1 partials
-    double d0 = 0.0, d1 = 0.0;
-    for (int b = b0 + warp; b < b1; b += W) {
-      const int rb = b << 5, row = rb + lane;
-      const double2* y = B[bi[Y]];
-      double2 k = gen_row(P.gen, P.params, b, t, [&](int c) { return y[c]; });
-      if (row < n) {
-        B[bi[K1]][row] = k;
-        const double2 yy = y[row];
-        const double sc = atol + rtol * cabs_(yy);
-        d0 += cnorm(make_double2(yy.x / sc, yy.y / sc));
-        d1 += cnorm(make_double2(k.x / sc, k.y / sc));
-      }
-    }
-    if (np) observe_pass<MODE>(P, B, bi, s_pend, np, h_last, obs_slots[obs_par], s_red, rank, G);
+    double d0, d1;
+    start_pass(P, c, s0, s1, &d0, &d1);
     d0 = block_sum(d0, s_red);
     d1 = block_sum(d1, s_red);
     if (threadIdx.x == 0) {
       red[static_cast<long long>(kSlotD0) * G + rank] = d0;
       red[static_cast<long long>(kSlotD1) * G + rank] = d1;
     }
+    if (c.np) observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
     grid_barrier(P.bar, G);
-    rhs_evals += 1;
-    if (np) {
-      observe_commit(P, s_pend, np, obs_slots[obs_par], G);
-      obs_par ^= 1;
-      np = 0;
-    }
-    d0 = sqrt(grid_value(red, kSlotD0, G, &s_val) / static_cast<double>(n));
-    d1 = sqrt(grid_value(red, kSlotD1, G, &s_val) / static_cast<double>(n));
-    double h0 = (d0 < 1e-5 || d1 < 1e-5) ? 1e-6 : 0.01 * d0 / d1;
-    h0 = fmin(h0, tf - t);
-    if (!(h0 > 0)) h0 = 1e-6;
-    // pass S2: k2 = G(t0+h0)(y + h0 k1) ; d2 partial
-    double d2 = 0.0;
-    for (int b = b0 + warp; b < b1; b += W) {
-      const int rb = b << 5, row = rb + lane;
-      const double2* y = B[bi[Y]];
-      const double2* k1 = B[bi[K1]];
-      double2 k = gen_row(P.gen, P.params, b, t + h0, [&](int c) {
-        const double2 a = y[c], b2 = k1[c];
-        return make_double2(a.x + h0 * b2.x, a.y + h0 * b2.y);
-      });
-      if (row < n) {
-        const double2 yy = y[row], kk1 = k1[row];
-        const double sc = atol + rtol * cabs_(yy);
-        const double2 df = csub(k, kk1);
-        d2 += cnorm(make_double2(df.x / sc, df.y / sc));
+    if (c.np) observe_commit(P, c, slots(c.obs_par), G);
+    grid_value(red, kSlotD0, G, &s_val[0]);
+    __syncthreads();
+    if (threadIdx.x == 0) s_val[1] = s_val[0];
+    __syncthreads();
+    grid_value(red, kSlotD1, G, &s_val[0]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (c.np) {
+        c.obs_par ^= 1;
+        c.np = 0;
       }
+      c.rhs_evals += 1;
+      const double dd0 = sqrt(s_val[1] / static_cast<double>(P.n));
+      const double dd1 = sqrt(s_val[0] / static_cast<double>(P.n));
+      double h0 = (dd0 < 1e-5 || dd1 < 1e-5) ? 1e-6 : 0.01 * dd0 / dd1;  // integrator.hpp:168-170
+      h0 = fmin(h0, P.tf - c.t);
+      if (!(h0 > 0)) h0 = 1e-6;
+      c.h0 = h0;
+      c.d1 = dd1;
     }
+    __syncthreads();
+    double d2 = start_pass2(P, c, s0, s1);
     d2 = block_sum(d2, s_red);
     if (threadIdx.x == 0) red[static_cast<long long>(kSlotD2) * G + rank] = d2;
     grid_barrier(P.bar, G);
-    rhs_evals += 1;
-    d2 = sqrt(grid_value(red, kSlotD2, G, &s_val) / static_cast<double>(n)) / h0;
-    double h1;
-    if (fmax(d1, d2) <= 1e-15) h1 = fmax(1e-6, h0 * 1e-3);
-    else h1 = pow(0.01 / fmax(d1, d2), 0.2);
-    h = fmin(fmin(100.0 * h0, h1), tf - t);
-  }
-
-  // ---------------- main loop (evolve.cpp:156-167) ----------------
-  while (next < P.n_ev && status == kRunning) {
-    if (steps >= P.max_steps) {
-      status = kFailMaxSteps;
-      fail_t = t;
-      break;
-    }
-    int attempts = 0;
-    for (;;) {  // Dopri5::step (integrator.hpp:78-147)
-      const double hh = fmin(h, tf - t);
-      const bool clamped = hh < h;
-      if (!(hh > 0.0)) { status = kFailPastEnd; fail_t = t; break; }
-      if (hh <= fabs(t) * 1e-15 + 1e-300) { status = kFailUnderflow; fail_t = t; break; }
-      if (++attempts > 1000) { status = kFailRejected; fail_t = t; break; }
-      ++attempts_total;
-      using namespace dp;
-      // ---- stage 2: k2 = G(t + c2 h)(y + h a21 k1); ysti3 -> SA
-      {
-        const double2* y = B[bi[Y]];
-        const double2* k1 = B[bi[K1]];
-        double2* k2o = B[bi[K2]];
-        double2* so = B[bi[SA]];
-        for (int b = b0 + warp; b < b1; b += W) {
-          const int rb = b << 5, row = rb + lane;
-          double2 k = gen_row(P.gen, P.params, b, t + c2 * hh, [&](int c) {
-            const double2 a = y[c], q = k1[c];
-            return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
-          });
-          if (row < n) {
-            const double2 yy = y[row], q1 = k1[row];
-            k2o[row] = k;
-            so[row] = make_double2(yy.x + hh * (a31 * q1.x + a32 * k.x), yy.y + hh * (a31 * q1.y + a32 * k.y));
-          }
-        }
-        if (np) observe_pass<MODE>(P, B, bi, s_pend, np, h_last, obs_slots[obs_par], s_red, rank, G);
-        grid_barrier(P.bar, G);
-        if (np) {
-          observe_commit(P, s_pend, np, obs_slots[obs_par], G);
-          obs_par ^= 1;
-          np = 0;
-        }
-      }
-      // ---- stage 3: k3 = G(t + c3 h) SA; ysti4 -> SB
-      {
-        const double2* y = B[bi[Y]];
-        const double2* x = B[bi[SA]];
-        const double2 *k1 = B[bi[K1]], *k2 = B[bi[K2]];
-        double2* ko = B[bi[K3]];
-        double2* so = B[bi[SB]];
-        for (int b = b0 + warp; b < b1; b += W) {
-          const int rb = b << 5, row = rb + lane;
-          double2 k = gen_row(P.gen, P.params, b, t + c3 * hh, [&](int c) { return x[c]; });
-          if (row < n) {
-            const double2 yy = y[row], q1 = k1[row], q2 = k2[row];
-            ko[row] = k;
-            so[row] = make_double2(yy.x + hh * (a41 * q1.x + a42 * q2.x + a43 * k.x),
-                                   yy.y + hh * (a41 * q1.y + a42 * q2.y + a43 * k.y));
-          }
-        }
-        grid_barrier(P.bar, G);
-      }
-      // ---- stage 4: k4 = G(t + c4 h) SB; ysti5 -> SA
-      {
-        const double2* y = B[bi[Y]];
-        const double2* x = B[bi[SB]];
-        const double2 *k1 = B[bi[K1]], *k2 = B[bi[K2]], *k3 = B[bi[K3]];
-        double2* ko = B[bi[K4]];
-        double2* so = B[bi[SA]];
-        for (int b = b0 + warp; b < b1; b += W) {
-          const int rb = b << 5, row = rb + lane;
-          double2 k = gen_row(P.gen, P.params, b, t + c4 * hh, [&](int c) { return x[c]; });
-          if (row < n) {
-            const double2 yy = y[row], q1 = k1[row], q2 = k2[row], q3 = k3[row];
-            ko[row] = k;
-            so[row] = make_double2(yy.x + hh * (a51 * q1.x + a52 * q2.x + a53 * q3.x + a54 * k.x),
-                                   yy.y + hh * (a51 * q1.y + a52 * q2.y + a53 * q3.y + a54 * k.y));
-          }
-        }
-        grid_barrier(P.bar, G);
-      }
-      // ---- stage 5: k5 = G(t + c5 h) SA; ysti6 -> SB
-      {
-        const double2* y = B[bi[Y]];
-        const double2* x = B[bi[SA]];
-        const double2 *k1 = B[bi[K1]], *k2 = B[bi[K2]], *k3 = B[bi[K3]], *k4 = B[bi[K4]];
-        double2* ko = B[bi[K5]];
-        double2* so = B[bi[SB]];
-        for (int b = b0 + warp; b < b1; b += W) {
-          const int rb = b << 5, row = rb + lane;
-          double2 k = gen_row(P.gen, P.params, b, t + c5 * hh, [&](int c) { return x[c]; });
-          if (row < n) {
-            const double2 yy = y[row], q1 = k1[row], q2 = k2[row], q3 = k3[row], q4 = k4[row];
-            ko[row] = k;
-            so[row] = make_double2(
-                yy.x + hh * (a61 * q1.x + a62 * q2.x + a63 * q3.x + a64 * q4.x + a65 * k.x),
-                yy.y + hh * (a61 * q1.y + a62 * q2.y + a63 * q3.y + a64 * q4.y + a65 * k.y));
-          }
-        }
-        grid_barrier(P.bar, G);
-      }
-      // ---- stage 6: k6 = G(t + h) SB; ysti7 (= y1 candidate) -> SA
-      {
-        const double2* y = B[bi[Y]];
-        const double2* x = B[bi[SB]];
-        const double2 *k1 = B[bi[K1]], *k3 = B[bi[K3]], *k4 = B[bi[K4]], *k5 = B[bi[K5]];
-        double2* ko = B[bi[K6]];
-        double2* so = B[bi[SA]];
-        for (int b = b0 + warp; b < b1; b += W) {
-          const int rb = b << 5, row = rb + lane;
-          double2 k = gen_row(P.gen, P.params, b, t + hh, [&](int c) { return x[c]; });
-          if (row < n) {
-            const double2 yy = y[row], q1 = k1[row], q3 = k3[row], q4 = k4[row], q5 = k5[row];
-            ko[row] = k;
-            so[row] = make_double2(
-                yy.x + hh * (a71 * q1.x + a73 * q3.x + a74 * q4.x + a75 * q5.x + a76 * k.x),
-                yy.y + hh * (a71 * q1.y + a73 * q3.y + a74 * q4.y + a75 * q5.y + a76 * k.y));
-          }
-        }
-        grid_barrier(P.bar, G);
-      }
-      // ---- stage 7 (FSAL): k7 = G(t + h) SA; embedded error partial
-      double err;
-      {
-        const double2* y = B[bi[Y]];
-        const double2* x = B[bi[SA]];
-        const double2 *k1 = B[bi[K1]], *k3 = B[bi[K3]], *k4 = B[bi[K4]], *k5 = B[bi[K5]], *k6 = B[bi[K6]];
-        double2* ko = B[bi[K7]];
-        double esq = 0.0;
-        for (int b = b0 + warp; b < b1; b += W) {
-          const int rb = b << 5, row = rb + lane;
-          double2 k = gen_row(P.gen, P.params, b, t + hh, [&](int c) { return x[c]; });
-          if (row < n) {
-            const double2 yy = y[row], y1 = x[row], q1 = k1[row], q3 = k3[row], q4 = k4[row],
-                          q5 = k5[row], q6 = k6[row];
-            ko[row] = k;
-            double2 e;
-            e.x = hh * (e1 * q1.x + e3 * q3.x + e4 * q4.x + e5 * q5.x + e6 * q6.x + e7 * k.x);
-            e.y = hh * (e1 * q1.y + e3 * q3.y + e4 * q4.y + e5 * q5.y + e6 * q6.y + e7 * k.y);
-            const double sc = atol + rtol * fmax(cabs_(yy), cabs_(y1));
-            const double qq = cabs_(e) / sc;
-            esq += qq * qq;
-          }
-        }
-        esq = block_sum(esq, s_red);
-        if (threadIdx.x == 0) red[static_cast<long long>(kSlotErr) * G + rank] = esq;
-        grid_barrier(P.bar, G);
-        err = sqrt(grid_value(red, kSlotErr, G, &s_val) / static_cast<double>(n));
-        if (!isfinite(err)) err = 10.0;
-      }
-      rhs_evals += 6;
-      if (err <= 1.0) {  // accept (integrator.hpp:119-142)
-        const double fac11 = pow(err, expo1);
-        double fac = fac11 / pow(facold, beta);
-        fac = fmax(facc2, fmin(facc1, fac / safe));
-        const double h_new = hh / fac;
-        facold = fmax(err, 1e-4);
-        t_old = t;
-        t += hh;
-        h_last = hh;
-        {  // y_old <- y, y <- ysti7, FSAL k1 <-> k7
-          const int oy = bi[Y], oyo = bi[YO];
-          bi[YO] = oy;
-          bi[Y] = bi[SA];
-          bi[SA] = oyo;
-          const int k1p = bi[K1];
-          bi[K1] = bi[K7];
-          bi[K7] = k1p;
-        }
-        ++steps;
-        if (!clamped) h = h_new;
-        else h = fmax(h, h_new);
-        break;
-      }
-      ++rejected;
-      h = hh / fmin(facc1, pow(err, expo1) / safe);
-    }
-    if (status != kRunning) break;
-    // observation events reached by this step (evolve.cpp:160-165)
-    for (;;) {
-      while (next < P.n_ev && P.ev_t[next] <= t + eps_t && np < kcap)
-        push_pending((fmin(P.ev_t[next], t) - t_old) / h_last);
-      const bool more = next < P.n_ev && P.ev_t[next] <= t + eps_t;
-      const bool last = t >= tf - eps_t;
-      if (!(more || (last && np))) break;
-      // flush now: either the pending list is full or the solve is ending
-      __syncthreads();
-      observe_pass<MODE>(P, B, bi, s_pend, np, h_last, obs_slots[obs_par], s_red, rank, G);
-      grid_barrier(P.bar, G);
-      observe_commit(P, s_pend, np, obs_slots[obs_par], G);
-      obs_par ^= 1;
-      np = 0;
+    grid_value(red, kSlotD2, G, &s_val[0]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      c.rhs_evals += 1;
+      const double dd2 = sqrt(s_val[0] / static_cast<double>(P.n)) / c.h0;  // :180-186
+      double h1;
+      if (fmax(c.d1, dd2) <= 1e-15) h1 = fmax(1e-6, c.h0 * 1e-3);
+      else h1 = pow(0.01 / fmax(c.d1, dd2), 0.2);
+      c.h = fmin(fmin(100.0 * c.h0, h1), P.tf - c.t);
     }
     __syncthreads();
-    if (t >= tf - eps_t) break;
   }
 
-  // trailing events observe the final state (evolve.cpp:169)
-  if (status == kRunning) {
-    if (np) {
-      __syncthreads();
-      observe_pass<MODE>(P, B, bi, s_pend, np, h_last, obs_slots[obs_par], s_red, rank, G);
-      grid_barrier(P.bar, G);
-      observe_commit(P, s_pend, np, obs_slots[obs_par], G);
-      obs_par ^= 1;
-      np = 0;
+  // ---------------- solve loop (evolve.cpp:156-167) ----------------
+  for (;;) {
+    if (threadIdx.x == 0) {
+      if (c.next >= P.n_ev) c.done = 1;
+      else begin_attempt(P, c);
     }
-    while (next < P.n_ev) {
-      while (next < P.n_ev && np < kcap) push_pending(__longlong_as_double(0x7ff8000000000000ll));
+    __syncthreads();
+    if (c.done || c.status != kRunning) break;
+    // stage 2 (+ observations of the previous accepted step)
+    stage_pass<2>(P, c, s0, s1);
+    if (c.np) observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
+    grid_barrier(P.bar, G);
+    if (c.np) {
+      observe_commit(P, c, slots(c.obs_par), G);
       __syncthreads();
-      observe_pass<MODE>(P, B, bi, s_pend, np, h_last, obs_slots[obs_par], s_red, rank, G);
-      grid_barrier(P.bar, G);
-      observe_commit(P, s_pend, np, obs_slots[obs_par], G);
-      obs_par ^= 1;
-      np = 0;
+      if (threadIdx.x == 0) {
+        c.obs_par ^= 1;
+        c.np = 0;
+      }
     }
-    status = kDone;
+    stage_pass<3>(P, c, s0, s1);
+    grid_barrier(P.bar, G);
+    stage_pass<4>(P, c, s0, s1);
+    grid_barrier(P.bar, G);
+    stage_pass<5>(P, c, s0, s1);
+    grid_barrier(P.bar, G);
+    stage_pass<6>(P, c, s0, s1);
+    grid_barrier(P.bar, G);
+    double esq = stage_pass<7>(P, c, s0, s1);
+    esq = block_sum(esq, s_red);
+    if (threadIdx.x == 0) red[static_cast<long long>(kSlotErr) * G + rank] = esq;
+    grid_barrier(P.bar, G);
+    grid_value(red, kSlotErr, G, &s_val[0]);
+    __syncthreads();
+    if (threadIdx.x == 0) finish_attempt(P, c, s_val[0], kcap);
+    __syncthreads();
+    while (c.flush) {  // pending list full, or the solve ends with events pending
+      flush_obs();
+      if (threadIdx.x == 0) {
+        while (c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t && c.np < kcap)
+          push_pending(P, c, (fmin(P.ev_t[c.next], c.t) - c.t_old) / c.h_last);
+        const bool more = c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t;
+        c.flush = more || (c.t >= P.tf - P.eps_t && c.np > 0);
+      }
+      __syncthreads();
+    }
+    if (c.done) break;
+  }
+
+  // ---------------- pending and trailing events observe the final state (evolve.cpp:169) ----
+  if (c.status == kRunning) {
+    if (c.np) flush_obs();
+    while (c.next < P.n_ev) {
+      if (threadIdx.x == 0)
+        while (c.next < P.n_ev && c.np < kcap) push_pending(P, c, __longlong_as_double(0x7ff8000000000000ll));
+      __syncthreads();
+      flush_obs();
+    }
   }
   if (rank == 0 && threadIdx.x == 0) {
-    GridCtl* c = P.ctl;
-    c->t = t;
-    c->h = h;
-    c->status = status;
-    c->fail_t = fail_t;
-    c->steps = steps;
-    c->rejected = rejected;
-    c->rhs_evals = rhs_evals;
-    c->attempts = attempts_total;
-    c->final_buf = bi[Y];
+    GridCtl* o = P.ctl;
+    o->t = c.t;
+    o->h = c.h;
+    o->status = c.status == kRunning ? kDone : c.status;
+    o->fail_t = c.fail_t;
+    o->steps = c.steps;
+    o->rejected = c.rejected;
+    o->rhs_evals = c.rhs_evals;
+    o->attempts = c.attempts_total;
+    o->final_buf = 0;
   }
 }
 
