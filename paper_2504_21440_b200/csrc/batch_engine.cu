@@ -31,6 +31,9 @@ constexpr int kThreads = 512;   // 16 warps
 constexpr int W = kThreads / 32;
 constexpr int RPW = 32 / B;     // rows per warp iteration
 constexpr int NBUF = 14;
+#ifndef QSG_BATCH_MINB
+#define QSG_BATCH_MINB 2
+#endif
 
 enum Buf { Y = 0, YO, K1, K1O, K2, K3, K4, K5, K6, K7, SA, SB, Y1, SC };
 enum Phase { FREE = 0, START, RUN, JUMP, OBS, FINISH, DONE };
@@ -208,7 +211,7 @@ __device__ bool has_more(const Slot& s, const BatchProblem& P) {
   return s.grid < P.n_t && (P.tlist[s.grid] <= s.obs_limit + P.eps_t || s.tail_src >= 0);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) batch_kernel(const __grid_constant__ BatchProblem P) {
+__global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const __grid_constant__ BatchProblem P) {
   __shared__ Slot S[B];
   __shared__ double sred[W * B * 15];
   __shared__ double sout[B * 15];
