@@ -273,29 +273,24 @@ def kerr_sweep_spmv(ctx, q, torch, dev, peak):
 def mcsolve_sharded(args, ctx, q, torch, ws, rank):
     """BASELINE configs[2] workload (TFIM-14 mcsolve) on a bounded trajectory count, sharded in
     contiguous blocks (trajectory i = RngStream(2025, i) on every N), NCCL all-gather of block sums."""
+    from paper_2504_21440_b200.dist import combine_mean, gather_block_sums, shard_range
+
     ntraj = args.mc_traj
     m = q.Model("ising", *TFIM_MC)
     G = q.Generator([ctx.op(m.export(q.SEL_MC_GEN))])
     cops = [m.export(q.SEL_C_OP, k) for k in range(m.n_cops)]
     eops = [m.export(q.SEL_E_OP, 2)]
-    b, e = ntraj * rank // ws, ntraj * (rank + 1) // ws
+    b, e = shard_range(ntraj, rank, ws)
     barrier(ws)
     r = q.mcsolve(ctx, G, cops, eops, m.dim, m.psi0(), TLIST, MC_SEED, b, e, per_traj=False)
     t_ms = allreduce_max(r["kernel_ms"], ws)
-    bs = r["block_sum"]
     if ws > 1:
-        import torch.distributed as dist
-        mine = torch.from_numpy(np.concatenate([bs.reshape(-1), [r["n_ok"]]]).astype(np.complex128)).cuda()
-        gathered = [torch.empty_like(mine) for _ in range(ws)]
-        dist.all_gather(gathered, mine)
-        parts = [g.cpu().numpy() for g in gathered]
-        sums = [p[:-1].reshape(bs.shape) for p in parts]
-        n_ok = int(sum(p[-1].real for p in parts))
-        ranges = [(ntraj * k // ws, ntraj * (k + 1) // ws) for k in range(ws)]
-        mean = q.ensemble_combine(ranges, sums, n_ok)
+        sums, counts = gather_block_sums(r["block_sum"], r["n_ok"], ws, device=torch.device("cuda", ctx.device))
+        n_ok = sum(counts)
+        mean = combine_mean(ntraj, ws, sums, counts)
     else:
         n_ok = r["n_ok"]
-        mean = bs / n_ok
+        mean = q.ensemble_combine([(0, ntraj)], [r["block_sum"]], n_ok)
     return {"workload": "mcsolve TFIM-14 (16384-dim), Sz_total, tlist linspace(0,10,100)",
             "ntraj": ntraj, "n_ok": n_ok, "device_s": t_ms / 1e3, "traj_per_s": ntraj / (t_ms / 1e3),
             "attempts_rank0": r["attempts"], "mean_Sz_t10": float(mean[0, -1].real),
