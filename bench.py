@@ -212,7 +212,9 @@ def run_ours(args, ws, rank, local):
                                  "frac": spmv_bytes / spmv_ms / 1e6 / peak, "bytes_model": "20*nnz+4*(n+1)+32*n"}}
     if not args.quick:
         secondary["kerr_sweep_spmv"] = kerr_sweep_spmv(ctx, q, torch, dev, peak)
+        secondary["kerr_cutoff_mesolve"] = kerr_cutoff_mesolve(ctx, q, peak)
         secondary["mcsolve"] = mcsolve_sharded(args, ctx, q, torch, ws, rank)
+        secondary["param_sweep"] = param_sweep_sharded(args, ctx, q, torch, ws, rank)
     del out, y
 
     line = {
@@ -268,6 +270,54 @@ def kerr_sweep_spmv(ctx, q, torch, dev, peak):
         b = 20 * Lk.nnz + 4 * (Lk.n_rows + 1) + 32 * Lk.n_rows
         out[f"N{N}"] = {"rows": Lk.n_rows, "nnz": Lk.nnz, "us": ms * 1e3, "GBps": b / ms / 1e6}
     return out
+
+
+def kerr_cutoff_mesolve(ctx, q, peak):
+    """BASELINE configs[3]: Kerr resonator mesolve over cutoffs N (Liouvillian up to 160k rows),
+    abstol 1e-8, tlist linspace(0,10,101); device time per solve and byte-model GB/s."""
+    out = {}
+    tl = np.linspace(0.0, 10.0, 101)
+    for N in (50, 100, 200, 400):
+        m = q.Model("kerr", N, 1.0, 0.01, 2.0, 1.0)
+        Lk = m.export(q.SEL_L_CONST)
+        g = q.Generator([ctx.op(Lk)])
+        eops = [m.export(q.SEL_E_OP, k) for k in range(m.n_eops)]
+        psi = m.psi0()
+        rho0 = np.outer(psi, psi.conj()).reshape(-1, order="F").copy()
+        q.mesolve(ctx, g, m.dim, rho0, tl, eops)  # warm-up
+        r = q.mesolve(ctx, g, m.dim, rho0, tl, eops)
+        n, nnz = Lk.n_rows, Lk.nnz
+        b = (6 * (20 * nnz + 4 * (n + 1)) + 47 * 16 * n) * r["attempts"]
+        out[f"N{N}"] = {"rows": n, "nnz": nnz, "solve_ms": r["kernel_ms"], "attempts": r["attempts"],
+                        "us_per_attempt": r["kernel_ms"] * 1e3 / r["attempts"], "GBps_model": b / r["kernel_ms"] / 1e6,
+                        "grid_ctas": r["grid_ctas"], "note": "L2-resident operator: GB/s can exceed the HBM rate"}
+    return out
+
+
+def param_sweep_sharded(args, ctx, q, torch, ws, rank):
+    """BASELINE configs[4]: 256 (Delta, F) points of two coupled Kerr modes (N=10 each,
+    U=0.1, J=0.5, gamma=1), Delta in linspace(-2,2,16) x F in linspace(0.1,1,16), one mesolve per
+    point, points sharded in contiguous blocks over ranks (no numeric reduction)."""
+    from paper_2504_21440_b200.dist import shard_range
+
+    m = q.Model("coupled_kerr", 10, 0.1, 0.5, 1.0)
+    ops = [ctx.op(m.export(q.SEL_L_CONST))] + [ctx.op(m.export(q.SEL_L_TERM, k)) for k in range(m.n_terms)]
+    g = q.Generator(ops, [(q.COEFF_CONST, 0, 0, 1.0, 0.0), (q.COEFF_PARAM, 0, 0, 0.0, 0.0),
+                          (q.COEFF_PARAM, 1, 0, 0.0, 0.0)])
+    eops = [m.export(q.SEL_E_OP, k) for k in range(m.n_eops)]
+    pts = np.array([[d, f] for d in np.linspace(-2, 2, 16) for f in np.linspace(0.1, 1.0, 16)])
+    b, e = shard_range(len(pts), rank, ws)
+    rho0 = np.zeros(m.dim * m.dim, complex)
+    rho0[0] = 1.0
+    tl = np.linspace(0.0, 10.0, 101)
+    q.mesolve_batch(ctx, g, m.dim, rho0, tl, eops, pts[b:b + 1])  # warm-up
+    barrier(ws)
+    r = q.mesolve_batch(ctx, g, m.dim, rho0, tl, eops, pts[b:e])
+    t_ms = allreduce_max(r["kernel_ms"], ws)
+    return {"workload": "256-point coupled-Kerr (N=10x10, Liouvillian 10^4 rows) mesolve sweep",
+            "points": len(pts), "points_this_rank": e - b, "device_s": t_ms / 1e3,
+            "points_per_s": len(pts) / (t_ms / 1e3), "attempts_rank0": r["attempts"],
+            "failed": int((r["status"] != 0).sum())}
 
 
 def mcsolve_sharded(args, ctx, q, torch, ws, rank):
