@@ -51,6 +51,7 @@ struct RunOut {
   double kernel_ms = 0;
   long long attempts = 0;
   int grid = 0;
+  bool grid_mode = false;
 };
 
 // Runs systems [sys_begin, sys_begin + n_sys) through the batch kernel and downloads outputs.
@@ -59,24 +60,38 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   cudaError_t ce;
   P.n_systems = n_sys;
   P.jump_cap = jump_cap;
-  const int per_sm = batch_max_blocks_per_sm();
+  // grid mode keeps one 32-slot batch L2-resident across the whole GPU; it needs enough rows
+  // per CTA to be worth the grid barriers. QSG_BATCH_MODE=grid|local overrides.
+  const size_t grid_ws = batch_work_stride(P.n, true) * sizeof(double2);
+  bool grid_mode = P.n >= 4096 && grid_ws <= static_cast<size_t>(ctx->l2_bytes) * 85 / 100;
+  if (const char* m = std::getenv("QSG_BATCH_MODE")) grid_mode = std::string(m) == "grid";
+  const int per_sm = batch_max_blocks_per_sm(grid_mode);
   if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "batch occupancy");
-  long long want = (n_sys + batch_slots() - 1) / batch_slots();
-  int grid = static_cast<int>(std::min<long long>(static_cast<long long>(per_sm) * ctx->sm_count, want));
+  int grid;
+  if (grid_mode) {
+    grid = std::min(per_sm * ctx->sm_count, (P.n + 31) / 32);
+  } else {
+    const long long want = (n_sys + batch_slots(false) - 1) / batch_slots(false);
+    grid = static_cast<int>(std::min<long long>(static_cast<long long>(per_sm) * ctx->sm_count, want));
+  }
   if (const char* eg = std::getenv("QSG_BATCH_GRID")) grid = std::max(1, std::min(grid, std::atoi(eg)));
   o.grid = grid;
-  const size_t stride = batch_work_stride(P.n);
-  DevBuf work, q, ex, st, ft, stt, jc, jt, jch, att;
+  o.grid_mode = grid_mode;
+  const size_t stride = batch_work_stride(P.n, grid_mode);
+  DevBuf work, q, ex, st, ft, stt, jc, jt, jch, att, gp, gf, gb;
   const size_t nvals = static_cast<size_t>(std::max(1, P.n_e)) * P.n_t;
-  if ((ce = work.alloc(stride * grid * sizeof(double2), s)) || (ce = q.alloc(8, s)) ||
+  if ((ce = work.alloc(stride * (grid_mode ? 1 : grid) * sizeof(double2), s)) || (ce = q.alloc(8, s)) ||
       (ce = ex.alloc(nvals * n_sys * sizeof(double2), s)) || (ce = st.alloc(sizeof(int) * n_sys, s)) ||
       (ce = ft.alloc(sizeof(double) * n_sys, s)) || (ce = stt.alloc(sizeof(long long) * 3 * n_sys, s)) ||
       (ce = jc.alloc(sizeof(int) * n_sys, s)) ||
       (ce = jt.alloc(sizeof(double) * std::max<long long>(1, n_sys * jump_cap), s)) ||
-      (ce = jch.alloc(sizeof(int) * std::max<long long>(1, n_sys * jump_cap), s)) || (ce = att.alloc(8, s)))
+      (ce = jch.alloc(sizeof(int) * std::max<long long>(1, n_sys * jump_cap), s)) || (ce = att.alloc(8, s)) ||
+      (ce = gp.alloc(sizeof(double) * 32 * 15 * grid, s)) || (ce = gf.alloc(sizeof(double) * 32 * 15, s)) ||
+      (ce = gb.alloc(2 * sizeof(unsigned), s)))
     return cuda_fail(ce, "batch workspace");
   cudaMemsetAsync(q.p, 0, 8, s);
   cudaMemsetAsync(att.p, 0, 8, s);
+  cudaMemsetAsync(gb.p, 0, 2 * sizeof(unsigned), s);
   cudaMemsetAsync(ex.p, 0, nvals * n_sys * sizeof(double2), s);
   cudaMemsetAsync(jc.p, 0, sizeof(int) * n_sys, s);
   P.work = work.as<double2>();
@@ -90,8 +105,11 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   P.jump_time = jt.as<double>();
   P.jump_channel = jch.as<int>();
   P.attempts_total = att.as<long long>();
+  P.gpart = gp.as<double>();
+  P.gfin = gf.as<double>();
+  P.bar = gb.as<unsigned>();
   cudaEventRecord(ctx->ev[2], s);
-  if ((ce = launch_batch(P, grid, s))) return cuda_fail(ce, "batch launch");
+  if ((ce = launch_batch(P, grid_mode, grid, s))) return cuda_fail(ce, "batch launch");
   cudaEventRecord(ctx->ev[3], s);
   o.expect.resize(nvals * n_sys);
   o.status.resize(n_sys);
@@ -157,7 +175,7 @@ extern "C" qsg_status qsg_mcsolve(qsg_ctx* ctx, const qsg_generator* G, int32_t 
     return QSG_INVALID_GRID;
   }
   if (n_c > kBatchMaxCops || n_e > kBatchMaxEops) {
-    set_error("TooLarge: mcsolve supports at most 32 collapse and 8 expectation operators");
+    set_error("TooLarge: mcsolve supports at most 24 collapse and 8 expectation operators");
     return QSG_TOO_LARGE;
   }
   cudaStream_t s = ctx->stream;
@@ -237,7 +255,7 @@ extern "C" qsg_status qsg_mcsolve(qsg_ctx* ctx, const qsg_generator* G, int32_t 
     timing->kernel_ms = o.kernel_ms;
     timing->attempts = o.attempts;
     timing->grid_ctas = o.grid;
-    timing->lanes = batch_slots();
+    timing->lanes = batch_slots(o.grid_mode);
   }
   return QSG_OK;
 }
@@ -313,7 +331,7 @@ extern "C" qsg_status qsg_mesolve_batch(qsg_ctx* ctx, const qsg_generator* L, in
     timing->kernel_ms = o.kernel_ms;
     timing->attempts = o.attempts;
     timing->grid_ctas = o.grid;
-    timing->lanes = batch_slots();
+    timing->lanes = batch_slots(o.grid_mode);
   }
   return status ? QSG_OK : rc;
 }

@@ -26,16 +26,18 @@ namespace qsg {
 
 namespace {
 
-constexpr int B = 8;            // slots per CTA
+constexpr int kMaxB = 32;       // slots per batch (B = 8 CTA-local, 32 grid-wide)
 constexpr int kThreads = 512;   // 16 warps
 constexpr int W = kThreads / 32;
-constexpr int RPW = 32 / B;     // rows per warp iteration
-constexpr int NBUF = 14;
+constexpr int NBUF = 12;
 #ifndef QSG_BATCH_MINB
 #define QSG_BATCH_MINB 2
 #endif
 
-enum Buf { Y = 0, YO, K1, K1O, K2, K3, K4, K5, K6, K7, SA, SB, Y1, SC };
+// Y1 (ysti7) shares SA and SC (collapsed state) shares SB: their live ranges never overlap for
+// a given slot (SA holds ysti5 until P4, ysti7 from P5 to the P7 commit; a JUMP slot writes SC in
+// P2 and consumes it in P3 while it runs no stages).
+enum Buf { Y = 0, YO, K1, K1O, K2, K3, K4, K5, K6, K7, SA, SB, Y1 = SA, SC = SB };
 enum Phase { FREE = 0, START, RUN, JUMP, OBS, FINISH, DONE };
 enum Src { SRC_DENSE = 0, SRC_Y = 1, SRC_SC = 2 };
 
@@ -91,17 +93,19 @@ __device__ double rng_uniform_pos(unsigned long long* s) {
   return u;
 }
 
+template <int BS>
 struct Ctx {
   const BatchProblem& P;
-  double2* w;  // CTA workspace
+  double2* w;  // batch workspace: NBUF arrays of [n][BS]
   int n;
-  __device__ double2* buf(int k) const { return w + static_cast<long long>(k) * n * B; }
-  __device__ double2 ld(int k, int r, int s) const { return buf(k)[static_cast<long long>(r) * B + s]; }
-  __device__ void st(int k, int r, int s, double2 v) const { buf(k)[static_cast<long long>(r) * B + s] = v; }
+  __device__ double2* buf(int k) const { return w + static_cast<long long>(k) * n * BS; }
+  __device__ double2 ld(int k, int r, int s) const { return buf(k)[static_cast<long long>(r) * BS + s]; }
+  __device__ void st(int k, int r, int s, double2 v) const { buf(k)[static_cast<long long>(r) * BS + s] = v; }
 };
 
 // dense output of slot s at index c (integrator.hpp:127-131,150-154) from the committed step
-__device__ __forceinline__ double2 dense_at(const Ctx& C, int c, int s, double theta, double h, int src) {
+template <int BS>
+__device__ __forceinline__ double2 dense_at(const Ctx<BS>& C, int c, int s, double theta, double h, int src) {
   if (src == SRC_Y) return C.ld(Y, c, s);
   if (src == SRC_SC) return C.ld(SC, c, s);
   using namespace dp;
@@ -158,25 +162,50 @@ __device__ __forceinline__ double2 gen_row_slot(const DevGen& g, const double* p
   return s;
 }
 
-// Deterministic per-slot reduction of NA accumulators: out[slot*NA + a] (shared memory).
-template <int NA>
-__device__ void slot_reduce(double (&acc)[NA], double* sred, double* out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, s = lane % B, rs = lane / B;
+__device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Deterministic per-slot reduction of NA accumulators -> out[slot*NA + a] (shared memory).
+// GRID: the CTA totals go to gpart[value][rank]; the last CTA to arrive sums every value over the
+// CTAs in rank order (so the result does not depend on arrival order), publishes gfin and
+// releases the others. Every CTA then holds identical totals.
+template <int BS, bool GRID, int NA>
+__device__ void slot_reduce(const BatchProblem& P, double (&acc)[NA], double* sred, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, s = lane % BS, rs = lane / BS;
 #pragma unroll
   for (int a = 0; a < NA; ++a)
 #pragma unroll
-    for (int off = B; off < 32; off <<= 1) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], off);
+    for (int off = BS; off < 32; off <<= 1) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], off);
   if (rs == 0)
 #pragma unroll
-    for (int a = 0; a < NA; ++a) sred[(warp * B + s) * NA + a] = acc[a];
+    for (int a = 0; a < NA; ++a) sred[(warp * BS + s) * NA + a] = acc[a];
   __syncthreads();
-  if (threadIdx.x < B * NA) {
+  if (threadIdx.x < BS * NA) {
     const int ss = threadIdx.x / NA, a = threadIdx.x % NA;
     double v = 0.0;
-    for (int w = 0; w < W; ++w) v += sred[(w * B + ss) * NA + a];
+    for (int w = 0; w < W; ++w) v += sred[(w * BS + ss) * NA + a];
     out[ss * NA + a] = v;
   }
   __syncthreads();
+  if constexpr (GRID) {
+    // two-phase distributed reduce: every CTA publishes its totals, then value i is summed over
+    // the CTAs in rank order by one warp of CTA (i mod G); a second barrier publishes the result.
+    const int G = gridDim.x, rank = blockIdx.x, cnt = BS * NA;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) P.gpart[static_cast<long long>(i) * G + rank] = out[i];
+    grid_barrier(P.bar, G);
+    for (int i = rank + warp * G; i < cnt; i += W * G) {
+      double v = 0.0;
+      for (int g = lane; g < G; g += 32) v += P.gpart[static_cast<long long>(i) * G + g];
+      v = warp_sum(v);
+      if (lane == 0) P.gfin[i] = v;
+    }
+    grid_barrier(P.bar, G);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) out[i] = P.gfin[i];
+    __syncthreads();
+  }
 }
 
 __device__ double params_at(const BatchProblem& P, const Slot& S, int i) {
@@ -211,34 +240,58 @@ __device__ bool has_more(const Slot& s, const BatchProblem& P) {
   return s.grid < P.n_t && (P.tlist[s.grid] <= s.obs_limit + P.eps_t || s.tail_src >= 0);
 }
 
+// BS slots per batch. !GRID: every CTA runs its own batch over all rows (block barriers only).
+// GRID: one batch for the whole cooperative grid, rows partitioned over CTAs, so the state of
+// the BS slots (NBUF x n x BS complex) stays L2-resident; passes are separated by grid barriers.
+template <int BS, bool GRID>
 __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const __grid_constant__ BatchProblem P) {
-  __shared__ Slot S[B];
-  __shared__ double sred[W * B * 15];
-  __shared__ double sout[B * 15];
+  constexpr int B = BS;
+  constexpr int RPW = 32 / BS;
+  __shared__ Slot S[BS];
+  extern __shared__ double sred[];  // W * BS * 15 (dynamic: up to 61 KB for the grid batch)
+  __shared__ double sout[BS * 15];
   __shared__ int s_alldone;
+  __shared__ long long s_next;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sl = lane % B, rs = lane / B;
   const int n = P.n;
-  const Ctx C{P, P.work + static_cast<long long>(blockIdx.x) * P.work_stride, n};
+  const Ctx<BS> C{P, P.work + (GRID ? 0LL : static_cast<long long>(blockIdx.x) * P.work_stride), n};
   const double atol = P.atol, rtol = P.rtol, eps_t = P.eps_t, tf = P.tf, t0 = P.t0;
+  const bool out_cta = !GRID || blockIdx.x == 0;  // the CTA that writes per-system outputs
+  const int rpc = GRID ? (n + gridDim.x - 1) / static_cast<int>(gridDim.x) : n;
+  const int r_lo = GRID ? min(n, static_cast<int>(blockIdx.x) * rpc) : 0;
+  const int r_hi = GRID ? min(n, r_lo + rpc) : n;
   auto rows = [&](auto&& f) {
-    for (int r = warp * RPW + rs; r < n; r += W * RPW) f(r);
+    for (int r = r_lo + warp * RPW + rs; r < r_hi; r += W * RPW) f(r);
   };
+  auto pass_sync = [&]() {
+    if constexpr (GRID) grid_barrier(P.bar, gridDim.x);
+    else __syncthreads();
+  };
+  auto reduce = [&](auto& acc) { slot_reduce<BS, GRID>(P, acc, sred, sout); };
 
   if (threadIdx.x < B) {
     S[threadIdx.x].phase = FREE;
     S[threadIdx.x].next_phase = FREE;
   }
+  if (threadIdx.x == 0) s_next = 0;
   __syncthreads();
 
   for (;;) {
     // ---------------- slot bookkeeping (one thread per slot) ----------------
+    if (GRID && threadIdx.x == 0) {  // deterministic assignment: identical in every CTA
+      for (int b = 0; b < B; ++b)
+        if (S[b].phase == FREE) S[b].sys = s_next < P.n_systems ? s_next++ : -1;
+    }
+    if (GRID) __syncthreads();
     if (threadIdx.x < B) {
       Slot& s = S[threadIdx.x];
       s.fresh = 0;
       if (s.phase == FREE) {
-        const unsigned long long idx = atomicAdd(P.queue, 1ull);
+        unsigned long long idx;
+        if (GRID) idx = s.sys < 0 ? ~0ull : static_cast<unsigned long long>(s.sys);
+        else idx = atomicAdd(P.queue, 1ull);
         if (idx < static_cast<unsigned long long>(P.n_systems)) {
           s.sys = static_cast<long long>(idx);
           s.phase = START;
@@ -307,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
     rows([&](int r) {
       if (S[sl].fresh) C.st(Y, r, sl, P.y0[r]);
     });
-    __syncthreads();
+    pass_sync();
 
     // ================= P1 =================
     {
@@ -335,7 +388,9 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
           C.st(SA, r, sl, make_double2(yy.x + hh * (a31 * q1.x + a32 * k.x), yy.y + hh * (a31 * q1.y + a32 * k.y)));
         });
       }
-      slot_reduce<2>(acc, sred, sout);
+      bool any_start = false;
+      for (int b = 0; b < B; ++b) any_start |= (S[b].phase == START);
+      if (any_start) reduce(acc);
       if (threadIdx.x < B && S[threadIdx.x].phase == START) {
         Slot& s = S[threadIdx.x];
         s.d0 = sqrt(sout[threadIdx.x * 2] / static_cast<double>(n));
@@ -349,46 +404,58 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       // ---- pending observations (every phase may carry some)
       int maxp = 0;
       for (int b = 0; b < B; ++b) maxp = max(maxp, S[b].phase == DONE ? 0 : S[b].n_pend);
-      for (int q = 0; q < maxp; ++q) {
-        const bool act = q < S[sl].n_pend && S[sl].phase != DONE;
-        const double th = act ? S[sl].pend_theta[q] : 0.0;
-        const int src = act ? S[sl].pend_src[q] : SRC_Y;
-        const double hl = S[sl].h_last;
-        for (int e = 0; e < P.n_e; ++e) {
-          double oa[3] = {0.0, 0.0, 0.0};
-          if (act) {
-            if (P.mode == 0) {  // <g|E g> / |g|^2 (trajectories.cpp:133-139)
-              rows([&](int r) {
-                const double2 ev = sell_row_slot(P.e_ops[e], r, [&](int c) { return dense_at(C, c, sl, th, hl, src); });
-                const double2 g = dense_at(C, r, sl, th, hl, src);
-                const double2 p = cmul(cconj(g), ev);
-                oa[0] += p.x;
-                oa[1] += p.y;
-                oa[2] += cnorm(g);
-              });
-            } else {  // sum A(i,j) rho_h(j,i) (evolve.cpp:286-295)
-              const int beg = P.eo_off[e], end = P.eo_off[e + 1];
-              for (int p = beg + warp * RPW + rs; p < end; p += W * RPW) {
-                const int i = P.eo_i[p], j = P.eo_j[p];
-                const double2 rji = dense_at(C, i * P.d + j, sl, th, hl, src);
-                const double2 rij = dense_at(C, j * P.d + i, sl, th, hl, src);
-                const double2 v = cmul(P.eo_v[p], cscale(0.5, cadd(rji, cconj(rij))));
-                oa[0] += v.x;
-                oa[1] += v.y;
-              }
+      const int npairs = maxp * P.n_e;
+      for (int c0 = 0; c0 < npairs; c0 += 5) {  // 5 (event, e_op) pairs x 3 values per reduction
+        double oa[15];
+#pragma unroll
+        for (int a = 0; a < 15; ++a) oa[a] = 0.0;
+#pragma unroll
+        for (int u = 0; u < 5; ++u) {
+          if (c0 + u >= npairs) continue;
+          const int q = (c0 + u) / P.n_e, e = (c0 + u) % P.n_e;
+          const bool act = q < S[sl].n_pend && S[sl].phase != DONE;
+          if (!act) continue;
+          const double th = S[sl].pend_theta[q];
+          const int src = S[sl].pend_src[q];
+          const double hl = S[sl].h_last;
+          if (P.mode == 0) {  // <g|E g> / |g|^2 (trajectories.cpp:133-139)
+            rows([&](int r) {
+              const double2 ev = sell_row_slot(P.e_ops[e], r, [&](int c) { return dense_at(C, c, sl, th, hl, src); });
+              const double2 g = dense_at(C, r, sl, th, hl, src);
+              const double2 pr = cmul(cconj(g), ev);
+              oa[3 * u] += pr.x;
+              oa[3 * u + 1] += pr.y;
+              oa[3 * u + 2] += cnorm(g);
+            });
+          } else {  // sum A(i,j) rho_h(j,i) (evolve.cpp:286-295)
+            const int beg = P.eo_off[e], end = P.eo_off[e + 1];
+            const int r0 = GRID ? beg + (end - beg) * static_cast<long long>(blockIdx.x) / gridDim.x : beg;
+            const int r1 = GRID ? beg + (end - beg) * static_cast<long long>(blockIdx.x + 1) / gridDim.x : end;
+            for (int k = r0 + warp * RPW + rs; k < r1; k += W * RPW) {
+              const int i = P.eo_i[k], j = P.eo_j[k];
+              const double2 rji = dense_at(C, i * P.d + j, sl, th, hl, src);
+              const double2 rij = dense_at(C, j * P.d + i, sl, th, hl, src);
+              const double2 v = cmul(P.eo_v[k], cscale(0.5, cadd(rji, cconj(rij))));
+              oa[3 * u] += v.x;
+              oa[3 * u + 1] += v.y;
             }
           }
-          slot_reduce<3>(oa, sred, sout);
-          if (threadIdx.x < B && q < S[threadIdx.x].n_pend && S[threadIdx.x].phase != DONE) {
-            Slot& s = S[threadIdx.x];
-            double2 v = make_double2(sout[threadIdx.x * 3], sout[threadIdx.x * 3 + 1]);
+        }
+        reduce(oa);
+        if (threadIdx.x < B && S[threadIdx.x].phase != DONE && out_cta) {
+          Slot& s = S[threadIdx.x];
+          for (int u = 0; u < 5 && c0 + u < npairs; ++u) {
+            const int q = (c0 + u) / P.n_e, e = (c0 + u) % P.n_e;
+            if (q >= s.n_pend) continue;
+            double2 v = make_double2(sout[threadIdx.x * 15 + 3 * u], sout[threadIdx.x * 15 + 3 * u + 1]);
             if (P.mode == 0) {
-              const double inv = 1.0 / sout[threadIdx.x * 3 + 2];
+              const double inv = 1.0 / sout[threadIdx.x * 15 + 3 * u + 2];
               v = make_double2(v.x * inv, v.y * inv);
             }
             P.expect[s.sys * P.n_e * P.n_t + static_cast<long long>(s.pend_grid[q]) * P.n_e + e] = v;
           }
         }
+        __syncthreads();
       }
       __syncthreads();
       // ---- jump weights |C_k g(jump_t)|^2 (trajectories.cpp:178-196), chunks of 8 channels
@@ -397,12 +464,14 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         for (int b = 0; b < B; ++b) anyj |= (S[b].phase == JUMP);
         if (anyj) {
           const double thj = (S[sl].jump_t - S[sl].t_old) / S[sl].h_last, hl = S[sl].h_last;
-          for (int k0 = 0; k0 < P.n_c; k0 += 8) {
-            double wa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          for (int k0 = 0; k0 < P.n_c; k0 += 15) {
+            double wa[15];
+#pragma unroll
+            for (int u = 0; u < 15; ++u) wa[u] = 0.0;
             if (ph == JUMP) {
               rows([&](int r) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
+                for (int u = 0; u < 15; ++u)
                   if (k0 + u < P.n_c) {
                     const double2 v = sell_row_slot(P.c_ops[k0 + u], r,
                                                     [&](int c) { return dense_at(C, c, sl, thj, hl, SRC_DENSE); });
@@ -410,9 +479,9 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
                   }
               });
             }
-            slot_reduce<8>(wa, sred, sout);
+            reduce(wa);
             if (threadIdx.x < B && S[threadIdx.x].phase == JUMP)
-              for (int u = 0; u < 8 && k0 + u < P.n_c; ++u) S[threadIdx.x].w[k0 + u] = sout[threadIdx.x * 8 + u];
+              for (int u = 0; u < 15 && k0 + u < P.n_c; ++u) S[threadIdx.x].w[k0 + u] = sout[threadIdx.x * 15 + u];
           }
           __syncthreads();
           if (threadIdx.x < B && S[threadIdx.x].phase == JUMP) {
@@ -432,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
               }
               if (ch == P.n_c) ch = P.n_c - 1;
               s.channel = ch;
-              if (s.njumps < P.jump_cap) {
+              if (out_cta && s.njumps < P.jump_cap) {
                 P.jump_time[s.sys * P.jump_cap + s.njumps] = s.jump_t;
                 P.jump_channel[s.sys * P.jump_cap + s.njumps] = ch;
               }
@@ -446,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         Slot& s = S[threadIdx.x];
         if (s.phase != DONE) s.n_pend = 0;
       }
-      __syncthreads();
+      pass_sync();
     }
 
     // ================= P2 =================
@@ -486,7 +555,9 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
           C.st(SC, r, sl, make_double2(v.x / nrm, v.y / nrm));
         });
       }
-      slot_reduce<1>(acc, sred, sout);
+      bool any_start = false;
+      for (int b = 0; b < B; ++b) any_start |= (S[b].phase == START);
+      if (any_start) reduce(acc);
       if (threadIdx.x < B && S[threadIdx.x].phase == START) {
         Slot& s = S[threadIdx.x];
         const double d2 = sqrt(sout[threadIdx.x] / static_cast<double>(n)) / s.h0;  // integrator.hpp:180-186
@@ -497,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         s.rhs_evals += 1;
         s.next_phase = RUN;
       }
-      __syncthreads();
+      pass_sync();
     }
 
     // ================= P3 =================
@@ -523,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
           C.st(Y, r, sl, C.ld(SC, r, sl));
         });
       }
-      __syncthreads();
+      pass_sync();
       if (threadIdx.x < B && S[threadIdx.x].phase == JUMP && S[threadIdx.x].next_phase == JUMP) {
         Slot& s = S[threadIdx.x];
         if (s.jump_t < tf - eps_t) {
@@ -558,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
                           yy.y + hh * (a61 * q1.y + a62 * q2.y + a63 * q3.y + a64 * q4.y + a65 * k.y)));
       });
     }
-    __syncthreads();
+    pass_sync();
     if (S[sl].phase == RUN) {
       const double* prm = slot_params(P, S[sl]);
       const double hh = S[sl].hh, t = S[sl].t;
@@ -573,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
                           yy.y + hh * (a71 * q1.y + a73 * q3.y + a74 * q4.y + a75 * q5.y + a76 * k.y)));
       });
     }
-    __syncthreads();
+    pass_sync();
 
     // ================= P6: stage 7 + embedded error =================
     {
@@ -596,7 +667,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
           acc[1] += cnorm(y1);
         });
       }
-      slot_reduce<2>(acc, sred, sout);
+      reduce(acc);
       if (threadIdx.x < B && S[threadIdx.x].phase == RUN) {
         Slot& s = S[threadIdx.x];
         using namespace dp;
@@ -604,7 +675,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         if (!isfinite(err)) err = 10.0;
         s.nrm2 = sout[threadIdx.x * 2 + 1];
         s.rhs_evals += 6;
-        atomicAdd(reinterpret_cast<unsigned long long*>(P.attempts_total), 1ull);
+        if (out_cta) atomicAdd(reinterpret_cast<unsigned long long*>(P.attempts_total), 1ull);
         if (err <= 1.0) {  // integrator.hpp:119-142
           const double fac11 = pow(err, expo1);
           double fac = fac11 / pow(s.facold, beta);
@@ -665,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       }
       bool anyc = false;
       for (int b = 0; b < B; ++b) anyc |= (S[b].phase == RUN && S[b].accepted && S[b].crossing);
-      if (anyc) slot_reduce<15>(g, sred, sout);
+      if (anyc) reduce(g);
       else __syncthreads();
       if (threadIdx.x < B && S[threadIdx.x].phase == RUN && S[threadIdx.x].accepted) {
         Slot& s = S[threadIdx.x];
@@ -713,12 +784,14 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
     if (threadIdx.x < B) {
       Slot& s = S[threadIdx.x];
       if (s.phase == FINISH) {  // its last observations were taken in this round's P1
-        P.status[s.sys] = s.status == kRunning ? kDone : s.status;
-        P.fail_t[s.sys] = s.t;
-        P.stats[s.sys * 3] = s.steps;
-        P.stats[s.sys * 3 + 1] = s.rejected;
-        P.stats[s.sys * 3 + 2] = s.rhs_evals;
-        P.jump_count[s.sys] = s.njumps;
+        if (out_cta) {
+          P.status[s.sys] = s.status == kRunning ? kDone : s.status;
+          P.fail_t[s.sys] = s.t;
+          P.stats[s.sys * 3] = s.steps;
+          P.stats[s.sys * 3 + 1] = s.rejected;
+          P.stats[s.sys * 3 + 2] = s.rhs_evals;
+          P.jump_count[s.sys] = s.njumps;
+        }
         s.next_phase = FREE;
       } else if (s.phase == OBS) {
         refill(s, P);
@@ -730,20 +803,48 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
   }
 }
 
-}  // namespace
+template <int BS, bool GRID>
+size_t dyn_smem() {
+  return static_cast<size_t>(W) * BS * 15 * sizeof(double);
+}
 
-int batch_slots() { return B; }
+template <int BS, bool GRID>
+void set_attrs() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(batch_kernel<BS, GRID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(dyn_smem<BS, GRID>()));
+    done = true;
+  }
+}
 
-size_t batch_work_stride(int n) { return static_cast<size_t>(NBUF) * static_cast<size_t>(n) * B; }
-
-int batch_max_blocks_per_sm() {
+template <int BS, bool GRID>
+int occupancy_of() {
+  set_attrs<BS, GRID>();
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, batch_kernel, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, batch_kernel<BS, GRID>, kThreads, dyn_smem<BS, GRID>());
   return nb;
 }
 
-cudaError_t launch_batch(const BatchProblem& P, int grid, cudaStream_t s) {
-  batch_kernel<<<grid, kThreads, 0, s>>>(P);
+}  // namespace
+
+int batch_slots(bool grid) { return grid ? kMaxB : 8; }
+
+size_t batch_work_stride(int n, bool grid) {
+  return static_cast<size_t>(NBUF) * static_cast<size_t>(n) * batch_slots(grid);
+}
+
+int batch_max_blocks_per_sm(bool grid) { return grid ? occupancy_of<kMaxB, true>() : occupancy_of<8, false>(); }
+
+cudaError_t launch_batch(const BatchProblem& P, bool grid_mode, int grid, cudaStream_t s) {
+  if (grid_mode) {
+    void* args[] = {const_cast<BatchProblem*>(&P)};
+    set_attrs<kMaxB, true>();
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(batch_kernel<kMaxB, true>), dim3(grid),
+                                       dim3(kThreads), args, dyn_smem<kMaxB, true>(), s);
+  }
+  set_attrs<8, false>();
+  batch_kernel<8, false><<<grid, kThreads, dyn_smem<8, false>(), s>>>(P);
   return cudaGetLastError();
 }
 

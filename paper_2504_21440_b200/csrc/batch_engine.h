@@ -8,7 +8,7 @@
 namespace qsg {
 
 constexpr int kBatchMaxPend = 6;   // observation events a slot can carry into one round
-constexpr int kBatchMaxCops = 32;  // collapse operators (mcsolve)
+constexpr int kBatchMaxCops = 24;  // collapse operators (mcsolve)
 constexpr int kBatchMaxEops = 8;   // expectation operators
 
 struct BatchProblem {
@@ -51,11 +51,15 @@ struct BatchProblem {
   int* jump_channel;
   int jump_cap;
   long long* attempts_total;  // accumulated device attempts (perf accounting)
+  // grid mode: deterministic cross-CTA slot reductions and pass barriers
+  double* gpart;  // (32 slots x 15 values) x G partials
+  double* gfin;   // 32 x 15 totals
+  unsigned* bar;  // {count, generation}
 };
 
-int batch_slots();
-cudaError_t launch_batch(const BatchProblem& P, int grid, cudaStream_t s);
-int batch_max_blocks_per_sm();
-size_t batch_work_stride(int n);  // double2 elements per CTA
+int batch_slots(bool grid);
+cudaError_t launch_batch(const BatchProblem& P, bool grid_mode, int grid, cudaStream_t s);
+int batch_max_blocks_per_sm(bool grid);
+size_t batch_work_stride(int n, bool grid);  // double2 elements per batch
 
 }  // namespace qsg

@@ -125,3 +125,53 @@ def test_mesolve_batch_sweep_parity(ctx):
         ex, st, _ = m.mesolve(t, params=prm)
         assert normwise_rel(res["expect"][p], ex) <= 1e-6, p
         assert_stats_close(res["stats"][p], st)
+
+
+@pytest.fixture(params=["local", "grid"])
+def batch_mode(request, monkeypatch):
+    """Both batch-engine layouts: per-CTA batches and the grid-wide L2-resident batch."""
+    monkeypatch.setenv("QSG_BATCH_MODE", request.param)
+    return request.param
+
+
+def test_both_modes_jc_parity(ctx, batch_mode):
+    m = O.Model("jc", 6, 1.0, 1.0, 0.1, 0.05, 0.05)
+    t = np.linspace(0, 60, 61)
+    dev = _mc(ctx, m, t, 7, 0, 40)
+    ref = m.mcsolve(t, 7, 40)
+    _compare_trajectories(dev, ref)
+
+
+def test_both_modes_threshold_crossing(ctx, batch_mode):
+    m = O.Model("decay2", 0.8)
+    r = _mc(ctx, m, np.linspace(0, 30, 31), 99, 0, 48, abstol=1e-13, reltol=1e-12)
+    for i in range(48):
+        u = O.rng(99, i, 2, 1)[0]
+        assert abs(np.exp(-0.8 * r["jumps"][i][0][0]) - u) < 5e-10
+
+
+def test_both_modes_ising_identical(ctx, monkeypatch):
+    """Grid-wide and per-CTA batches give the same per-trajectory records (TFIM-7 chain)."""
+    m = O.Model("ising", 7, 1, 1.0, 0.2, 1.0, 1)
+    t = np.linspace(0, 10, 100)
+    out = {}
+    for mode in ("local", "grid"):
+        monkeypatch.setenv("QSG_BATCH_MODE", mode)
+        out[mode] = _mc(ctx, m, t, 2025, 0, 40)
+    # same trajectories; only the reduction order differs (jump times agree to ~1e-13)
+    _compare_trajectories(out["grid"], out["local"], jt_tol=1e-9, ex_tol=1e-9, allow_diverged=1)
+    ref = m.mcsolve(t, 2025, 40)
+    _compare_trajectories(out["grid"], ref, allow_diverged=1)
+
+
+def test_both_modes_sweep(ctx, batch_mode):
+    m = O.Model("coupled_kerr", 4, 0.1, 0.5, 1.0)
+    gen = oracle_generator(ctx, m, "me")
+    t = np.linspace(0, 10, 101)
+    pts = np.array([[-1.0, 0.3], [0.5, 0.9], [2.0, 0.1]])
+    rho0 = np.zeros(m.dim * m.dim, complex)
+    rho0[0] = 1.0
+    res = q.mesolve_batch(ctx, gen, m.dim, rho0, t, e_ops_csr(m), pts)
+    for p, prm in enumerate(pts):
+        ex, st, _ = m.mesolve(t, params=prm)
+        assert normwise_rel(res["expect"][p], ex) <= 1e-6
