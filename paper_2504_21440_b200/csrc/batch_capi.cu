@@ -62,8 +62,13 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   P.jump_cap = jump_cap;
   // grid mode keeps one 32-slot batch L2-resident across the whole GPU; it needs enough rows
   // per CTA to be worth the grid barriers. QSG_BATCH_MODE=grid|local overrides.
+  // Measured on TFIM-14 (profiles/r01_summary.md): the grid batch wins while per-CTA batches
+  // would leave the GPU half empty (64 trajectories: 0.20 s vs 2.9 s); for large ensembles the
+  // per-CTA batches stream more work per barrier (2368 trajectories: 484 vs 312 traj/s).
   const size_t grid_ws = batch_work_stride(P.n, true) * sizeof(double2);
-  bool grid_mode = P.n >= 4096 && grid_ws <= static_cast<size_t>(ctx->l2_bytes) * 85 / 100;
+  const long long local_slots = static_cast<long long>(batch_max_blocks_per_sm(false)) * ctx->sm_count * batch_slots(false);
+  bool grid_mode = P.n >= 4096 && grid_ws <= static_cast<size_t>(ctx->l2_bytes) * 85 / 100 &&
+                   n_sys < local_slots * 5 / 8;
   if (const char* m = std::getenv("QSG_BATCH_MODE")) grid_mode = std::string(m) == "grid";
   const int per_sm = batch_max_blocks_per_sm(grid_mode);
   if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "batch occupancy");
