@@ -121,6 +121,12 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out);
 void qsg_op_destroy(qsg_op* op);
 int64_t qsg_op_nnz(const qsg_op* op);
 int64_t qsg_op_rows(const qsg_op* op);
+/* Storage of the operator store: 0 = plain SELL-32 (int32 column + complex128 value per entry),
+ * 1 / 2 = dictionary-coded SELL-32 (uint8 / uint16 code into the operator's distinct
+ * (column - row, value) pairs; lossless). qsg_op_dict_size: distinct pairs (0 when plain).
+ * Set QSG_NO_COMPRESS=1 to force the plain store. */
+int32_t qsg_op_code_bytes(const qsg_op* op);
+int32_t qsg_op_dict_size(const qsg_op* op);
 
 /* out = G(t) y  — SparseGenerator::apply (evolve.cpp:63-69). y/out: n complex. */
 qsg_status qsg_generator_apply(qsg_ctx* ctx, const qsg_generator* g, const double* params,

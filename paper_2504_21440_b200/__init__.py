@@ -506,3 +506,13 @@ class Model:
         return {"mean": mean.reshape(nt, ne).T.copy(), "per_traj": per.reshape(ntraj, nt, ne).transpose(0, 2, 1).copy(),
                 "stats": tuple(int(x) for x in st), "njumps": nj, "jumps": jumps, "failed": nf.value,
                 "kernel_ms": ms.value}
+
+
+def op_storage(op: "Operator"):
+    """(code_bytes, dictionary size) of an operator store: 0 = plain SELL-32, 1/2 = coded."""
+    L = lib()
+    L.qsg_op_code_bytes.restype = C.c_int32
+    L.qsg_op_code_bytes.argtypes = [P]
+    L.qsg_op_dict_size.restype = C.c_int32
+    L.qsg_op_dict_size.argtypes = [P]
+    return L.qsg_op_code_bytes(op._h), L.qsg_op_dict_size(op._h)

@@ -25,8 +25,7 @@ qsg_status make_sell(qsg_ctx* ctx, const qsg_csr& a, TmpOps& keep, DevSell& out)
   qsg_op* op = nullptr;
   if (qsg_status s = qsg_op_create(ctx, &a, &op)) return s;
   keep.ops.push_back(op);
-  out = DevSell{op->slice_off, op->rowlen, op->col, op->val, static_cast<int>(op->n_rows),
-                static_cast<int>(op->n_cols), op->nnz};
+  out = sell_view(op, false);
   return QSG_OK;
 }
 
@@ -152,7 +151,7 @@ qsg_status common_setup(qsg_ctx* ctx, const qsg_generator* G, long long n, const
     return QSG_UNSUPPORTED;
   }
   P.n = static_cast<int>(n);
-  P.gen = make_devgen(G);
+  P.gen = make_devgen(G, false);
   P.atol = opts ? opts->abstol : 1e-8;
   P.rtol = opts ? opts->reltol : 1e-6;
   if (!(P.atol > 0 && P.rtol > 0)) {

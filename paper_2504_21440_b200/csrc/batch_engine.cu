@@ -124,29 +124,53 @@ __device__ __forceinline__ double2 dense_at(const Ctx<BS>& C, int c, int s, doub
   return o;
 }
 
-// one row of a SELL operator applied to slot s of a gathered vector
+// one row of a SELL operator applied to slot s of a gathered vector (plain or dictionary-coded
+// store, engine.cuh DevSell); the row's entries are broadcast to the slots of the warp
 template <class XF>
 __device__ __forceinline__ double2 sell_row_slot(const DevSell& A, int row, XF&& xf) {
   const int sl = row >> 5, ln = row & 31;
   const int len = __ldg(A.rowlen + row);
-  const long long base = __ldg(A.slice_off + sl) * 32 + ln;
   double2 acc = make_double2(0.0, 0.0);
-  for (int j = 0; j < len; j += 4) {
-    int c[4];
-    double2 v[4];
+  if (A.code_bytes == 0) {
+    const long long base = __ldg(A.slice_off + sl) * 32 + ln;
+    for (int j = 0; j < len; j += 4) {
+      int c[4];
+      double2 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (j + u < len) {
-        c[u] = __ldg(A.col + base + 32LL * (j + u));
-        v[u] = __ldg(A.val + base + 32LL * (j + u));
-      } else {
-        c[u] = 0;
-        v[u] = make_double2(0.0, 0.0);
+      for (int u = 0; u < 4; ++u) {
+        if (j + u < len) {
+          c[u] = __ldg(A.col + base + 32LL * (j + u));
+          v[u] = __ldg(A.val + base + 32LL * (j + u));
+        } else {
+          c[u] = 0;
+          v[u] = make_double2(0.0, 0.0);
+        }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (j + u < len) cfma(v[u], xf(c[u]), acc);
+      for (int u = 0; u < 4; ++u)
+        if (j + u < len) cfma(v[u], xf(c[u]), acc);
+    }
+  } else {
+    const long long cb = __ldg(A.code_off + sl);
+    const int wp = static_cast<int>((__ldg(A.code_off + sl + 1) - cb) >> 5);
+    const long long base = cb + static_cast<long long>(ln) * wp;
+    for (int j = 0; j < len; j += 8) {
+      uint4 w;
+      if (A.code_bytes == 1) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(A.code8 + base + j));
+        w = make_uint4(v.x, v.y, 0u, 0u);
+      } else {
+        w = __ldg(reinterpret_cast<const uint4*>(A.code16 + base + j));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j + u < len) {
+          unsigned k;
+          if (A.code_bytes == 1) k = ((u < 4 ? w.x : w.y) >> (8 * (u & 3))) & 0xffu;
+          else k = ((u < 2 ? w.x : u < 4 ? w.y : u < 6 ? w.z : w.w) >> (16 * (u & 1))) & 0xffffu;
+          cfma(__ldg(A.dict_val + k), xf(row + __ldg(A.dict_off + k)), acc);
+        }
+    }
   }
   return acc;
 }

@@ -21,11 +21,20 @@ constexpr int kMaxTerms = 8;
 struct DevSell {
   const long long* slice_off;  // n_slices + 1, in units of 32-entry columns
   const int* rowlen;           // n_slices * 32 (0 for rows past n)
-  const int* col;              // 32 * slice_off[n_slices]
+  const int* col;              // 32 * slice_off[n_slices] (plain store)
   const double2* val;
   int n_rows;
   int n_cols;
   long long nnz;
+  // Dictionary-coded store (code_bytes 1 or 2): entry = code into (diagonal offset, value) pairs;
+  // column = row + dict_off[code], value = dict_val[code]. Lossless: every distinct pair of the
+  // operator is in the dictionary. code_bytes 0 = plain (col, val) store.
+  int code_bytes;
+  const long long* code_off;  // n_slices + 1, in entries: slice s holds 32 rows x Wp codes, row-contiguous
+  const unsigned char* code8;
+  const unsigned short* code16;
+  const int* dict_off;
+  const double2* dict_val;
 };
 
 struct DevCoeff {
@@ -121,29 +130,80 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+__device__ __forceinline__ uint2 ld_stream_u2(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // One row of a SELL-32 operator times a gathered vector (lane-per-row). XF maps col -> x[col].
 // Entries are consumed in ascending column order, as Eigen's CSC product accumulates a row.
 template <class XF>
 __device__ __forceinline__ double2 sell_row(const DevSell& A, int slice, int lane, XF&& xf) {
   const int len = __ldg(A.rowlen + slice * 32 + lane);
   const long long base = __ldg(A.slice_off + slice) * 32 + lane;
+  const int row = slice * 32 + lane;
   double2 acc = make_double2(0.0, 0.0);
-  for (int j = 0; j < len; j += 8) {
-    int c[8];
-    double2 v[8];
+  if (A.code_bytes == 0) {
+    for (int j = 0; j < len; j += 8) {
+      int c[8];
+      double2 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (j + u < len) {
-        c[u] = ld_stream(A.col + base + 32LL * (j + u));
-        v[u] = ld_stream(A.val + base + 32LL * (j + u));
-      } else {
-        c[u] = 0;
-        v[u] = make_double2(0.0, 0.0);
+      for (int u = 0; u < 8; ++u) {
+        if (j + u < len) {
+          c[u] = ld_stream(A.col + base + 32LL * (j + u));
+          v[u] = ld_stream(A.val + base + 32LL * (j + u));
+        } else {
+          c[u] = 0;
+          v[u] = make_double2(0.0, 0.0);
+        }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (j + u < len) cfma(v[u], xf(c[u]), acc);
+      for (int u = 0; u < 8; ++u)
+        if (j + u < len) cfma(v[u], xf(c[u]), acc);
+    }
+  } else {
+    // coded store: the row's codes are contiguous (Wp per row, a multiple of 8), so 8 codes come
+    // in one 8 B (uint8) or 16 B (uint16) load and a 32-entry row is in flight after 4 loads
+    const long long cb = __ldg(A.code_off + slice);
+    const int wp = static_cast<int>((__ldg(A.code_off + slice + 1) - cb) >> 5);
+    const long long base = cb + static_cast<long long>(lane) * wp;
+    for (int j0 = 0; j0 < len; j0 += 32) {
+      uint4 w[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = j0 + 8 * c;
+        if (j < len) {
+          if (A.code_bytes == 1) {
+            const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + j));
+            w[c] = make_uint4(v.x, v.y, 0u, 0u);
+          } else {
+            w[c] = ld_stream_u4(reinterpret_cast<const uint4*>(A.code16 + base + j));
+          }
+        } else {
+          w[c] = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = j0 + 8 * c + u;
+          if (j < len) {
+            unsigned k;
+            if (A.code_bytes == 1) k = ((u < 4 ? w[c].x : w[c].y) >> (8 * (u & 3))) & 0xffu;
+            else k = ((u < 2 ? w[c].x : u < 4 ? w[c].y : u < 6 ? w[c].z : w[c].w) >> (16 * (u & 1))) & 0xffffu;
+            cfma(__ldg(A.dict_val + k), xf(row + __ldg(A.dict_off + k)), acc);
+          }
+        }
+    }
   }
   return acc;
 }

@@ -170,7 +170,10 @@ __device__ __forceinline__ void push_pending(const GridProblem& P, Ctl& c, doubl
 
 // One fused stage pass: k_S = G(ts) x over this CTA's slices, then the stage epilogue
 // (integrator.hpp:91-102 for S = 2..6; error partial of :106-116 for S = 7).
-template <int S>
+// PF: load the epilogue operands before the SpMV (their HBM latency then overlaps the gathers).
+// Used with the dictionary-coded store, whose SpMV needs few registers; with the plain store the
+// extra live registers spill, so the operands are loaded after the SpMV instead.
+template <int S, bool PF>
 __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c, int s0, int s1) {
   using namespace dp;
   const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -182,8 +185,22 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
   const double2* __restrict__ k1 = c.p[K1];
   const double2* __restrict__ x = S == 2 ? nullptr : (S == 3 || S == 5 || S == 7) ? c.p[SA] : c.p[SB];
   double esq = 0.0;
+  const double2 z = make_double2(0.0, 0.0);
   for (int b = s0 + warp; b < s1; b += W) {
     const int row = (b << 5) + lane;
+    const bool ok = row < n;
+    double2 yy, q1, q2, q3, q4, q5, q6, y1;
+    auto load_operands = [&]() {
+      yy = ok ? y[row] : z;
+      q1 = ok ? k1[row] : z;
+      q2 = (S >= 3 && S <= 5 && ok) ? c.p[K2][row] : z;
+      q3 = (S >= 4 && ok) ? c.p[K3][row] : z;
+      q4 = (S >= 5 && ok) ? c.p[K4][row] : z;
+      q5 = (S >= 6 && ok) ? c.p[K5][row] : z;
+      q6 = (S == 7 && ok) ? c.p[K6][row] : z;
+      y1 = (S == 7 && ok) ? x[row] : z;
+    };
+    if (PF) load_operands();
     double2 k;
     if (S == 2)
       k = gen_row(P.gen, P.params, b, ts, [&](int col) {
@@ -192,33 +209,28 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
       });
     else
       k = gen_row(P.gen, P.params, b, ts, [&](int col) { return x[col]; });
-    if (row >= n) continue;
-    const double2 yy = y[row], q1 = k1[row];
+    if (!ok) continue;
+    if (!PF) load_operands();
     if (S == 2) {
       c.p[K2][row] = k;
       c.p[SA][row] = make_double2(yy.x + hh * (a31 * q1.x + a32 * k.x), yy.y + hh * (a31 * q1.y + a32 * k.y));
     } else if (S == 3) {
-      const double2 q2 = c.p[K2][row];
       c.p[K3][row] = k;
       c.p[SB][row] = make_double2(yy.x + hh * (a41 * q1.x + a42 * q2.x + a43 * k.x),
                                   yy.y + hh * (a41 * q1.y + a42 * q2.y + a43 * k.y));
     } else if (S == 4) {
-      const double2 q2 = c.p[K2][row], q3 = c.p[K3][row];
       c.p[K4][row] = k;
       c.p[SA][row] = make_double2(yy.x + hh * (a51 * q1.x + a52 * q2.x + a53 * q3.x + a54 * k.x),
                                   yy.y + hh * (a51 * q1.y + a52 * q2.y + a53 * q3.y + a54 * k.y));
     } else if (S == 5) {
-      const double2 q2 = c.p[K2][row], q3 = c.p[K3][row], q4 = c.p[K4][row];
       c.p[K5][row] = k;
       c.p[SB][row] = make_double2(yy.x + hh * (a61 * q1.x + a62 * q2.x + a63 * q3.x + a64 * q4.x + a65 * k.x),
                                   yy.y + hh * (a61 * q1.y + a62 * q2.y + a63 * q3.y + a64 * q4.y + a65 * k.y));
     } else if (S == 6) {
-      const double2 q3 = c.p[K3][row], q4 = c.p[K4][row], q5 = c.p[K5][row];
       c.p[K6][row] = k;
       c.p[SA][row] = make_double2(yy.x + hh * (a71 * q1.x + a73 * q3.x + a74 * q4.x + a75 * q5.x + a76 * k.x),
                                   yy.y + hh * (a71 * q1.y + a73 * q3.y + a74 * q4.y + a75 * q5.y + a76 * k.y));
     } else {
-      const double2 y1 = x[row], q3 = c.p[K3][row], q4 = c.p[K4][row], q5 = c.p[K5][row], q6 = c.p[K6][row];
       c.p[K7][row] = k;
       double2 e;
       e.x = hh * (e1 * q1.x + e3 * q3.x + e4 * q4.x + e5 * q5.x + e6 * q6.x + e7 * k.x);
@@ -337,7 +349,7 @@ __device__ void finish_attempt(const GridProblem& P, Ctl& c, double err_sq, int 
   }
 }
 
-template <int MODE>
+template <int MODE, bool PF>
 __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const __grid_constant__ GridProblem P) {
   __shared__ double s_red[kThreads / 32];
   __shared__ double s_val[2];
@@ -438,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     __syncthreads();
     if (c.done || c.status != kRunning) break;
     // stage 2 (+ observations of the previous accepted step)
-    stage_pass<2>(P, c, s0, s1);
+    stage_pass<2, PF>(P, c, s0, s1);
     if (c.np) observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
     grid_barrier(P.bar, G);
     if (c.np) {
@@ -449,15 +461,15 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
         c.np = 0;
       }
     }
-    stage_pass<3>(P, c, s0, s1);
+    stage_pass<3, PF>(P, c, s0, s1);
     grid_barrier(P.bar, G);
-    stage_pass<4>(P, c, s0, s1);
+    stage_pass<4, PF>(P, c, s0, s1);
     grid_barrier(P.bar, G);
-    stage_pass<5>(P, c, s0, s1);
+    stage_pass<5, PF>(P, c, s0, s1);
     grid_barrier(P.bar, G);
-    stage_pass<6>(P, c, s0, s1);
+    stage_pass<6, PF>(P, c, s0, s1);
     grid_barrier(P.bar, G);
-    double esq = stage_pass<7>(P, c, s0, s1);
+    double esq = stage_pass<7, PF>(P, c, s0, s1);
     esq = block_sum(esq, s_red);
     if (threadIdx.x == 0) red[static_cast<long long>(kSlotErr) * G + rank] = esq;
     grid_barrier(P.bar, G);
@@ -502,17 +514,17 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
   }
 }
 
-template <int MODE>
+template <int MODE, bool PF>
 cudaError_t launch_one(const GridProblem& P, int grid, cudaStream_t s) {
   void* args[] = {const_cast<GridProblem*>(&P)};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dp5_grid_kernel<MODE>), dim3(grid),
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dp5_grid_kernel<MODE, PF>), dim3(grid),
                                      dim3(kThreads), args, 0, s);
 }
 
-template <int MODE>
+template <int MODE, bool PF>
 int occupancy_one() {
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp5_grid_kernel<MODE>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp5_grid_kernel<MODE, PF>, kThreads, 0);
   return nb;
 }
 
@@ -520,10 +532,14 @@ int occupancy_one() {
 
 int grid_threads() { return kThreads; }
 
-int grid_max_blocks_per_sm(int mode) { return mode == 0 ? occupancy_one<0>() : occupancy_one<1>(); }
+int grid_max_blocks_per_sm(int mode, bool pf) {
+  if (mode == 0) return pf ? occupancy_one<0, true>() : occupancy_one<0, false>();
+  return pf ? occupancy_one<1, true>() : occupancy_one<1, false>();
+}
 
-cudaError_t launch_grid_dp5(const GridProblem& P, int mode, int grid, cudaStream_t s) {
-  return mode == 0 ? launch_one<0>(P, grid, s) : launch_one<1>(P, grid, s);
+cudaError_t launch_grid_dp5(const GridProblem& P, int mode, bool pf, int grid, cudaStream_t s) {
+  if (mode == 0) return pf ? launch_one<0, true>(P, grid, s) : launch_one<0, false>(P, grid, s);
+  return pf ? launch_one<1, true>(P, grid, s) : launch_one<1, false>(P, grid, s);
 }
 
 }  // namespace qsg

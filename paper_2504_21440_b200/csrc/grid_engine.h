@@ -51,7 +51,7 @@ struct GridProblem {
 };
 
 int grid_threads();
-int grid_max_blocks_per_sm(int mode);
-cudaError_t launch_grid_dp5(const GridProblem& P, int mode, int grid, cudaStream_t s);
+int grid_max_blocks_per_sm(int mode, bool pf);
+cudaError_t launch_grid_dp5(const GridProblem& P, int mode, bool pf, int grid, cudaStream_t s);
 
 }  // namespace qsg

@@ -38,13 +38,29 @@ cudaError_t upload(DevBuf& b, const void* src, size_t bytes, cudaStream_t s) {
   return cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyDefault, s);
 }
 
-DevGen make_devgen(const qsg_generator* g) {
+DevSell sell_view(const qsg_op* op, bool use_codes) {
+  DevSell v{};
+  v.slice_off = op->slice_off;
+  v.rowlen = op->rowlen;
+  v.col = op->col;
+  v.val = op->val;
+  v.n_rows = static_cast<int>(op->n_rows);
+  v.n_cols = static_cast<int>(op->n_cols);
+  v.nnz = op->nnz;
+  v.code_bytes = use_codes ? op->code_bytes : 0;
+  v.code_off = op->code_off;
+  v.code8 = op->code_bytes == 1 ? static_cast<const unsigned char*>(op->code) : nullptr;
+  v.code16 = op->code_bytes == 2 ? static_cast<const unsigned short*>(op->code) : nullptr;
+  v.dict_off = op->dict_off;
+  v.dict_val = op->dict_val;
+  return v;
+}
+
+DevGen make_devgen(const qsg_generator* g, bool use_codes) {
   DevGen d{};
   d.n_terms = g->n_terms;
   for (int k = 0; k < g->n_terms; ++k) {
-    const qsg_op* op = g->ops[k];
-    d.A[k] = DevSell{op->slice_off, op->rowlen, op->col, op->val, static_cast<int>(op->n_rows),
-                     static_cast<int>(op->n_cols), op->nnz};
+    d.A[k] = sell_view(g->ops[k], use_codes);
     if (k > 0 && g->coeffs) {
       const qsg_coeff& c = g->coeffs[k];
       d.c[k] = DevCoeff{c.kind, c.i, c.j, c.re, c.im};
@@ -193,6 +209,74 @@ __global__ void sell_fill_kernel(const int* rowptr, const int* col, const double
     scol[base + 32LL * k] = col[b + k];
     sval[base + 32LL * k] = val[b + k];
   }
+}
+
+// codes of row r at code_off[slice] + (r % 32) * Wp + k, Wp = slice width rounded up to 8
+template <class T>
+__global__ void sell_code_fill_kernel(const int* rowptr, const T* codes, int n, const long long* code_off, T* scode) {
+  const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int b = rowptr[r], e = rowptr[r + 1];
+  const long long cb = code_off[r >> 5];
+  const long long wp = (code_off[(r >> 5) + 1] - cb) >> 5;
+  const long long base = cb + (r & 31) * wp;
+  for (int k = 0; k < e - b; ++k) scode[base + k] = codes[b + k];
+}
+
+// Distinct (column - row, value) pairs of a host CSR operator, or an empty result when there are
+// more than 65535 (the plain store is used then). Open addressing on the exact bit patterns.
+struct PairDict {
+  std::vector<int> off;
+  std::vector<double2> val;
+  std::vector<unsigned short> code;  // per CSR entry
+  bool ok = false;
+};
+
+static PairDict build_pair_dict(const qsg_csr* a) {
+  PairDict d;
+  const long long nnz = a->nnz;
+  constexpr unsigned kCap = 1u << 18;  // table slots (>= 4x the largest dictionary)
+  std::vector<int> slot_id(kCap, -1);
+  std::vector<unsigned long long> kre, kim;
+  std::vector<int> koff;
+  d.code.resize(static_cast<size_t>(nnz));
+  for (long long r = 0; r < a->n_rows; ++r) {
+    for (int p = a->rowptr[r]; p < a->rowptr[r + 1]; ++p) {
+      const int off = a->col[p] - static_cast<int>(r);
+      unsigned long long re, im;
+      std::memcpy(&re, a->val + 2 * p, 8);
+      std::memcpy(&im, a->val + 2 * p + 1, 8);
+      unsigned long long h = re * 0x9E3779B97F4A7C15ULL ^ (im + 0x632BE59BD9B4E019ULL) * 0xBF58476D1CE4E5B9ULL ^
+                             static_cast<unsigned long long>(static_cast<unsigned>(off)) * 0x94D049BB133111EBULL;
+      h ^= h >> 29;
+      unsigned s = static_cast<unsigned>(h) & (kCap - 1);
+      for (;;) {
+        const int id = slot_id[s];
+        if (id < 0) {
+          if (koff.size() >= 65535) return PairDict{};
+          slot_id[s] = static_cast<int>(koff.size());
+          koff.push_back(off);
+          kre.push_back(re);
+          kim.push_back(im);
+          d.code[static_cast<size_t>(p)] = static_cast<unsigned short>(koff.size() - 1);
+          break;
+        }
+        if (koff[static_cast<size_t>(id)] == off && kre[static_cast<size_t>(id)] == re && kim[static_cast<size_t>(id)] == im) {
+          d.code[static_cast<size_t>(p)] = static_cast<unsigned short>(id);
+          break;
+        }
+        s = (s + 1) & (kCap - 1);
+      }
+    }
+  }
+  d.off = koff;
+  d.val.resize(koff.size());
+  for (size_t i = 0; i < koff.size(); ++i) {
+    std::memcpy(&d.val[i].x, &kre[i], 8);
+    std::memcpy(&d.val[i].y, &kim[i], 8);
+  }
+  d.ok = true;
+  return d;
 }
 
 // ---- RNG kernel (rng.cpp:14-47) ---------------------------------------------------------------
@@ -363,7 +447,9 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   }
   const int lanes = 1;
   const int threads = grid_threads();
-  const int per_sm = grid_max_blocks_per_sm(mode);
+  bool pf = true;  // prefetching stage variant when every term uses the coded store
+  for (int k = 0; k < G->n_terms; ++k) pf = pf && G->ops[k]->code_bytes > 0;
+  const int per_sm = grid_max_blocks_per_sm(mode, pf);
   if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "occupancy");
   const int max_grid = per_sm * ctx->sm_count;
   const long long nblk = (n + 31) / 32;
@@ -380,7 +466,7 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   P.red = d_red.as<double>();
   P.bar = d_bar.as<unsigned>();
   cudaEventRecord(ctx->ev[0], s);
-  if ((ce = launch_grid_dp5(P, mode, grid, s))) return cuda_fail(ce, "solver launch");
+  if ((ce = launch_grid_dp5(P, mode, pf, grid, s))) return cuda_fail(ce, "solver launch");
   cudaEventRecord(ctx->ev[1], s);
   GridCtl ctl{};
   if ((ce = cudaMemcpyAsync(&ctl, d_ctl.p, sizeof(GridCtl), cudaMemcpyDeviceToHost, s)))
@@ -526,12 +612,64 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
     qsg_op_destroy(op);
     return cuda_fail(e, "operator store build");
   }
+  // dictionary-coded store when the operator has few distinct (diagonal offset, value) pairs
+  const char* nc = std::getenv("QSG_NO_COMPRESS");
+  if (!(nc && nc[0] == '1') && a->nnz > 0 && !is_device_ptr(a->col) && !is_device_ptr(a->val) &&
+      !is_device_ptr(a->rowptr)) {
+    PairDict pd = build_pair_dict(a);
+    if (pd.ok) {
+      const int cb = pd.off.size() <= 256 ? 1 : 2;
+      DevBuf d_codes;
+      std::vector<unsigned char> c8;
+      const void* src = pd.code.data();
+      if (cb == 1) {
+        c8.assign(pd.code.begin(), pd.code.end());
+        src = c8.data();
+      }
+      const size_t cbytes = static_cast<size_t>(a->nnz) * cb;
+      std::vector<long long> coff(nsl + 1, 0);
+      for (long long i = 0; i < nsl; ++i) coff[i + 1] = coff[i] + 32 * ((w[i] + 7) / 8 * 8);
+      const size_t pc = static_cast<size_t>(std::max<long long>(1, coff[nsl]));
+      if ((e = upload(d_codes, src, cbytes, s)) || (e = cudaMalloc(&op->code, pc * cb)) ||
+          (e = cudaMalloc(&op->code_off, sizeof(long long) * (nsl + 1))) ||
+          (e = cudaMalloc(&op->dict_off, sizeof(int) * pd.off.size())) ||
+          (e = cudaMalloc(&op->dict_val, sizeof(double2) * pd.val.size()))) {
+        qsg_op_destroy(op);
+        return cuda_fail(e, "coded operator store");
+      }
+      cudaMemsetAsync(op->code, 0, pc * cb, s);
+      cudaMemcpyAsync(op->code_off, coff.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(op->dict_off, pd.off.data(), sizeof(int) * pd.off.size(), cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(op->dict_val, pd.val.data(), sizeof(double2) * pd.val.size(), cudaMemcpyHostToDevice, s);
+      const unsigned nb = static_cast<unsigned>((n + 255) / 256);
+      if (cb == 1)
+        sell_code_fill_kernel<unsigned char><<<nb, 256, 0, s>>>(d_rp.as<int>(), d_codes.as<unsigned char>(),
+                                                                static_cast<int>(n), op->code_off,
+                                                                static_cast<unsigned char*>(op->code));
+      else
+        sell_code_fill_kernel<unsigned short><<<nb, 256, 0, s>>>(d_rp.as<int>(), d_codes.as<unsigned short>(),
+                                                                 static_cast<int>(n), op->code_off,
+                                                                 static_cast<unsigned short*>(op->code));
+      if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(s))) {
+        qsg_op_destroy(op);
+        return cuda_fail(e, "coded operator store build");
+      }
+      op->code_bytes = cb;
+      op->dict_n = static_cast<int>(pd.off.size());
+      // the plain entries stay resident too: the batched engine reads them (its operator is
+      // L2-resident, where the code -> dictionary indirection only adds latency)
+    }
+  }
   *out = op;
   return QSG_OK;
 }
 
 void qsg_op_destroy(qsg_op* op) {
   if (!op) return;
+  cudaFree(op->code);
+  cudaFree(op->code_off);
+  cudaFree(op->dict_off);
+  cudaFree(op->dict_val);
   cudaFree(op->slice_off);
   cudaFree(op->rowlen);
   cudaFree(op->col);
@@ -540,6 +678,9 @@ void qsg_op_destroy(qsg_op* op) {
 }
 
 int64_t qsg_op_nnz(const qsg_op* op) { return op ? op->nnz : 0; }
+
+int32_t qsg_op_code_bytes(const qsg_op* op) { return op ? op->code_bytes : -1; }
+int32_t qsg_op_dict_size(const qsg_op* op) { return op ? op->dict_n : -1; }
 int64_t qsg_op_rows(const qsg_op* op) { return op ? op->n_rows : 0; }
 
 qsg_status qsg_generator_apply(qsg_ctx* ctx, const qsg_generator* g, const double* params,

@@ -31,7 +31,18 @@ struct qsg_op {
   int* col = nullptr;
   double2* val = nullptr;
   int max_rowlen = 0;
+  // dictionary-coded entries (engine.cuh DevSell): 0 = plain, 1 = uint8, 2 = uint16 codes
+  int code_bytes = 0;
+  long long* code_off = nullptr;  // per slice, in entries (row-contiguous code blocks)
+  void* code = nullptr;
+  int* dict_off = nullptr;
+  double2* dict_val = nullptr;
+  int dict_n = 0;
 };
+
+namespace qsg {
+DevSell sell_view(const qsg_op* op, bool use_codes = true);
+}
 
 namespace qsg {
 
@@ -62,7 +73,7 @@ struct DevBuf {
 // Upload host-or-device array into a fresh device buffer.
 cudaError_t upload(DevBuf& b, const void* src, size_t bytes, cudaStream_t s);
 
-DevGen make_devgen(const qsg_generator* g);
+DevGen make_devgen(const qsg_generator* g, bool use_codes = true);
 qsg_status check_generator(const qsg_generator* g, long long n);
 qsg_status check_tlist(const double* tlist, long long n_t);
 

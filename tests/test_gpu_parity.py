@@ -136,3 +136,22 @@ def test_invalid_tlist(ctx):
     assert ei.value.code == 11
     with pytest.raises(q.QsgError):
         q.mesolve(ctx, gen, m.dim, rho0_vec(m), [0.0, 2.0, 1.0], e_ops_csr(m))
+
+
+@pytest.mark.parametrize("compress", ["1", "0"])
+def test_operator_store_formats_agree(ctx, monkeypatch, compress):
+    """Plain and dictionary-coded SELL stores give the same SpMV and the same solve."""
+    monkeypatch.setenv("QSG_NO_COMPRESS", "0" if compress == "1" else "1")
+    m = O.Model("ising", 3, 2, 1.0, 0.2, 1.0, 1)
+    gen = oracle_generator(ctx, m, "me")
+    cb, nd = q.op_storage(gen.ops[0])
+    assert (cb > 0) == (compress == "1"), (cb, nd)
+    rng = np.random.default_rng(5)
+    y = rng.standard_normal(gen.n) + 1j * rng.standard_normal(gen.n)
+    dev = q.generator_apply(ctx, gen, y)
+    ref = m.generator_apply(O.L_CONST, 0.0, y)
+    assert np.max(np.abs(dev - ref)) <= 1e-13 * np.max(np.abs(ref))
+    t = np.linspace(0, 4, 41)
+    res = q.mesolve(ctx, gen, m.dim, rho0_vec(m), t, e_ops_csr(m))
+    ex, st, _ = m.mesolve(t)
+    assert normwise_rel(res["expect"], ex) <= TOL
