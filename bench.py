@@ -174,16 +174,19 @@ def run_ours(args, ws, rank, local):
     att = attempts[-1]
     stats = r["stats"]
 
-    # ---- roofline of the fused DP5 kernel (SURVEY.md §8d byte model, per launch = per solve)
-    b_att = 6 * (20 * nnz + 4 * (n + 1)) + 47 * 16 * n
-    b_init = 2 * (20 * nnz + 4 * (n + 1)) + 6 * 16 * n
+    # ---- roofline of the fused DP5 kernel, per launch (= per solve). Byte model of SURVEY.md §8d
+    # with the operator-store term of the format actually read.
+    cb, ndict = q.op_storage(op)
+    mat_bytes = store_bytes(cb, ndict, n, nnz)
+    b_att = 6 * mat_bytes + 47 * 16 * n
+    b_init = 2 * mat_bytes + 6 * 16 * n
     alg_bytes = b_att * att + b_init
     achieved = alg_bytes / (ms_step / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "dp5_grid_kernel_dram_bytes.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            traffic = json.load(open(tp)).get("coded" if cb else "plain", {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -192,6 +195,9 @@ def run_ours(args, ws, rank, local):
     Lh = q.CsrMatrix(pin(L.rowptr), pin(L.col), pin(L.val), L.n_rows, L.n_cols)
     rho0_h = pin(rho0)
     e2e_steps = max(1, min(args.steps, 3))
+    op_w = ctx.op(Lh)  # untimed warm-up of the upload / store-build path
+    q.mesolve(ctx, q.Generator([op_w]), d, rho0_h, TLIST, eops)
+    op_w.close()
     barrier(ws)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
@@ -203,13 +209,32 @@ def run_ours(args, ws, rank, local):
     h2d = csr_bytes(L) + rho0.nbytes + sum(csr_bytes(e) for e in eops)
     d2h = r2["expect"].nbytes
 
-    # ---- secondary: plain SpMV of the operator store (SpMV HBM GB/s metric)
+    # ---- secondary: SpMV of the operator store (SpMV HBM GB/s metric), and the same solve on the
+    # plain (int32 column + complex128 value) store for comparison
     y = torch.randn(n, dtype=torch.complex128, device=f"cuda:{dev}")
     out = torch.empty_like(y)
     spmv_ms = q.generator_apply_timed(ctx, gen, y, out, reps=20)
-    spmv_bytes = 20 * nnz + 4 * (n + 1) + 32 * n
-    secondary = {"spmv_tfim10": {"ms": spmv_ms, "GBps": spmv_bytes / spmv_ms / 1e6,
-                                 "frac": spmv_bytes / spmv_ms / 1e6 / peak, "bytes_model": "20*nnz+4*(n+1)+32*n"}}
+    spmv_bytes = mat_bytes + 32 * n
+    secondary = {"spmv_tfim10": {"store": "coded" if cb else "plain", "ms": spmv_ms,
+                                 "GBps": spmv_bytes / spmv_ms / 1e6, "frac": spmv_bytes / spmv_ms / 1e6 / peak,
+                                 "bytes_model": "store bytes + 32*n"}}
+    os.environ["QSG_NO_COMPRESS"] = "1"
+    op_p = ctx.op(L)
+    del os.environ["QSG_NO_COMPRESS"]
+    gen_p = q.Generator([op_p])
+    q.mesolve(ctx, gen_p, d, rho0_dev, TLIST, eops)
+    kp = [q.mesolve(ctx, gen_p, d, rho0_dev, TLIST, eops) for _ in range(max(1, min(args.steps, 3)))]
+    ms_p = sum(x["kernel_ms"] for x in kp) / len(kp)
+    mat_p = store_bytes(0, 0, n, nnz)
+    alg_p = (6 * mat_p + 47 * 16 * n) * kp[-1]["attempts"] + 2 * mat_p + 6 * 16 * n
+    spmv_p = q.generator_apply_timed(ctx, gen_p, y, out, reps=20)
+    secondary["plain_store"] = {
+        "solve_ms": ms_p, "GBps": alg_p / ms_p / 1e6, "frac": alg_p / ms_p / 1e6 / peak,
+        "spmv_ms": spmv_p, "spmv_GBps": (mat_p + 32 * n) / spmv_p / 1e6,
+        "bytes_model": "per attempt 6*(20*nnz+4*n+8*n/32) + 47*16*n"}
+    op_p.close()
+    secondary["operator_store"] = {"code_bytes": cb, "dict_pairs": ndict, "bytes_per_spmv": mat_bytes,
+                                   "plain_bytes_per_spmv": mat_p}
     if not args.quick:
         secondary["kerr_sweep_spmv"] = kerr_sweep_spmv(ctx, q, torch, dev, peak)
         secondary["kerr_cutoff_mesolve"] = kerr_cutoff_mesolve(ctx, q, peak)
@@ -243,7 +268,9 @@ def run_ours(args, ws, rank, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": "dp5_grid_kernel (persistent fused DP5 solve, 1 launch per solve)",
-                     "bytes_model": "per attempt 6*(20*nnz+4*(n+1)) + 47*16*n (SURVEY.md 8d) + start 2 SpMV"},
+                     "bytes_model": "per attempt 6*store + 47*16*n (SURVEY.md 8d vector passes) + start 2 SpMV; "
+                                    "store = code_bytes*nnz + 4*n + 16*n/32 + 20*pairs (coded) or "
+                                    "20*nnz + 4*n + 8*n/32 (plain)"},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "path": "qsg_op_create(pinned host CSR) + qsg_mesolve(host rho0 -> host expect)"},
         "gpu_launches": args.steps,
@@ -254,6 +281,15 @@ def run_ours(args, ws, rank, local):
         line["cpu_baseline"] = cpu_baseline(att)
     ctx.close()
     return line
+
+
+def store_bytes(code_bytes, dict_pairs, n, nnz):
+    """Bytes one SpMV reads from the operator store (SELL-32): entries + row lengths + slice
+    offsets (+ the (offset, value) dictionary of a coded store)."""
+    nsl = (n + 31) // 32
+    if code_bytes:
+        return code_bytes * nnz + 4 * n + 16 * nsl + 20 * dict_pairs
+    return 20 * nnz + 4 * n + 8 * nsl
 
 
 def kerr_sweep_spmv(ctx, q, torch, dev, peak):
@@ -267,7 +303,8 @@ def kerr_sweep_spmv(ctx, q, torch, dev, peak):
         y = torch.randn(Lk.n_rows, dtype=torch.complex128, device=f"cuda:{dev}")
         o = torch.empty_like(y)
         ms = q.generator_apply_timed(ctx, g, y, o, reps=50)
-        b = 20 * Lk.nnz + 4 * (Lk.n_rows + 1) + 32 * Lk.n_rows
+        cbk, ndk = q.op_storage(g.ops[0])
+        b = store_bytes(cbk, ndk, Lk.n_rows, Lk.nnz) + 32 * Lk.n_rows
         out[f"N{N}"] = {"rows": Lk.n_rows, "nnz": Lk.nnz, "us": ms * 1e3, "GBps": b / ms / 1e6}
     return out
 
@@ -287,7 +324,8 @@ def kerr_cutoff_mesolve(ctx, q, peak):
         q.mesolve(ctx, g, m.dim, rho0, tl, eops)  # warm-up
         r = q.mesolve(ctx, g, m.dim, rho0, tl, eops)
         n, nnz = Lk.n_rows, Lk.nnz
-        b = (6 * (20 * nnz + 4 * (n + 1)) + 47 * 16 * n) * r["attempts"]
+        cbk, ndk = q.op_storage(g.ops[0])
+        b = (6 * store_bytes(cbk, ndk, n, nnz) + 47 * 16 * n) * r["attempts"]
         out[f"N{N}"] = {"rows": n, "nnz": nnz, "solve_ms": r["kernel_ms"], "attempts": r["attempts"],
                         "us_per_attempt": r["kernel_ms"] * 1e3 / r["attempts"], "GBps_model": b / r["kernel_ms"] / 1e6,
                         "grid_ctas": r["grid_ctas"], "note": "L2-resident operator: GB/s can exceed the HBM rate"}

@@ -223,60 +223,153 @@ __global__ void sell_code_fill_kernel(const int* rowptr, const T* codes, int n, 
   for (int k = 0; k < e - b; ++k) scode[base + k] = codes[b + k];
 }
 
-// Distinct (column - row, value) pairs of a host CSR operator, or an empty result when there are
-// more than 65535 (the plain store is used then). Open addressing on the exact bit patterns.
-struct PairDict {
-  std::vector<int> off;
-  std::vector<double2> val;
-  std::vector<unsigned short> code;  // per CSR entry
-  bool ok = false;
-};
+// ---- dictionary of distinct (column - row, value) pairs, built on the device -------------------
+// Lock-free open addressing: a 64-bit signature claims a slot by CAS, the owner then publishes the
+// full key; equal signatures are confirmed against the full key (exact bit patterns), so the
+// dictionary is lossless. Dense ids follow slot order, which depends only on the keys.
+constexpr unsigned kDictSlots = 1u << 17;
 
-static PairDict build_pair_dict(const qsg_csr* a) {
-  PairDict d;
-  const long long nnz = a->nnz;
-  constexpr unsigned kCap = 1u << 18;  // table slots (>= 4x the largest dictionary)
-  std::vector<int> slot_id(kCap, -1);
-  std::vector<unsigned long long> kre, kim;
-  std::vector<int> koff;
-  d.code.resize(static_cast<size_t>(nnz));
-  for (long long r = 0; r < a->n_rows; ++r) {
-    for (int p = a->rowptr[r]; p < a->rowptr[r + 1]; ++p) {
-      const int off = a->col[p] - static_cast<int>(r);
-      unsigned long long re, im;
-      std::memcpy(&re, a->val + 2 * p, 8);
-      std::memcpy(&im, a->val + 2 * p + 1, 8);
-      unsigned long long h = re * 0x9E3779B97F4A7C15ULL ^ (im + 0x632BE59BD9B4E019ULL) * 0xBF58476D1CE4E5B9ULL ^
-                             static_cast<unsigned long long>(static_cast<unsigned>(off)) * 0x94D049BB133111EBULL;
-      h ^= h >> 29;
-      unsigned s = static_cast<unsigned>(h) & (kCap - 1);
-      for (;;) {
-        const int id = slot_id[s];
-        if (id < 0) {
-          if (koff.size() >= 65535) return PairDict{};
-          slot_id[s] = static_cast<int>(koff.size());
-          koff.push_back(off);
-          kre.push_back(re);
-          kim.push_back(im);
-          d.code[static_cast<size_t>(p)] = static_cast<unsigned short>(koff.size() - 1);
-          break;
+__device__ __forceinline__ unsigned long long pair_sig(int off, unsigned long long re, unsigned long long im) {
+  unsigned long long h = re * 0x9E3779B97F4A7C15ULL ^ (im + 0x632BE59BD9B4E019ULL) * 0xBF58476D1CE4E5B9ULL ^
+                         static_cast<unsigned long long>(static_cast<unsigned>(off)) * 0x94D049BB133111EBULL;
+  h ^= h >> 29;
+  h *= 0xD6E8FEB86659FD93ULL;
+  h ^= h >> 32;
+  return h | 1ull;
+}
+
+__global__ void dict_insert_kernel(const int* rowptr, const int* col, const double2* val, int n,
+                                   unsigned long long* tsig, int* toff, double2* tval, int* ready,
+                                   unsigned* slot_of, int* overflow) {
+  const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int p = rowptr[r]; p < rowptr[r + 1]; ++p) {
+    const int off = col[p] - static_cast<int>(r);
+    const double2 v = val[p];
+    const unsigned long long re = __double_as_longlong(v.x), im = __double_as_longlong(v.y);
+    const unsigned long long sg = pair_sig(off, re, im);
+    unsigned slot = static_cast<unsigned>(sg >> 20) & (kDictSlots - 1);
+    bool placed = false;
+    for (unsigned probe = 0; probe < kDictSlots && !placed; ++probe) {
+      const unsigned long long prev = atomicCAS(tsig + slot, 0ull, sg);
+      if (prev == 0ull) {
+        toff[slot] = off;
+        tval[slot] = v;
+        __threadfence();
+        atomicExch(ready + slot, 1);
+        slot_of[p] = slot;
+        placed = true;
+      } else if (prev == sg) {
+        while (atomicAdd(ready + slot, 0) == 0) {
         }
-        if (koff[static_cast<size_t>(id)] == off && kre[static_cast<size_t>(id)] == re && kim[static_cast<size_t>(id)] == im) {
-          d.code[static_cast<size_t>(p)] = static_cast<unsigned short>(id);
-          break;
+        __threadfence();
+        const volatile int* vo = toff + slot;
+        const volatile double* vv = reinterpret_cast<const volatile double*>(tval + slot);
+        if (*vo == off && __double_as_longlong(vv[0]) == static_cast<long long>(re) &&
+            __double_as_longlong(vv[1]) == static_cast<long long>(im)) {
+          slot_of[p] = slot;
+          placed = true;
         }
-        s = (s + 1) & (kCap - 1);
       }
+      slot = (slot + 1) & (kDictSlots - 1);
     }
+    if (!placed) atomicExch(overflow, 1);
   }
-  d.off = koff;
-  d.val.resize(koff.size());
-  for (size_t i = 0; i < koff.size(); ++i) {
-    std::memcpy(&d.val[i].x, &kre[i], 8);
-    std::memcpy(&d.val[i].y, &kim[i], 8);
+}
+
+// one block: dense ids in slot order, dictionary arrays, and the number of distinct pairs
+__global__ void __launch_bounds__(1024) dict_compact_kernel(const unsigned long long* tsig, const int* toff,
+                                                            const double2* tval, unsigned* dense, int* dict_off,
+                                                            double2* dict_val, int dict_cap, int* count) {
+  __shared__ int part[1024];
+  constexpr unsigned per = kDictSlots / 1024;
+  const unsigned t = threadIdx.x, lo = t * per;
+  int c = 0;
+  for (unsigned i = 0; i < per; ++i) c += tsig[lo + i] != 0ull;
+  part[t] = c;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {  // inclusive scan
+    const int v = t >= static_cast<unsigned>(o) ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
   }
-  d.ok = true;
-  return d;
+  int id = part[t] - c;
+  for (unsigned i = 0; i < per; ++i)
+    if (tsig[lo + i] != 0ull) {
+      dense[lo + i] = static_cast<unsigned>(id);
+      if (id < dict_cap) {
+        dict_off[id] = toff[lo + i];
+        dict_val[id] = tval[lo + i];
+      }
+      ++id;
+    }
+  if (t == 1023) *count = part[1023];
+}
+
+template <class T>
+__global__ void sell_code_fill_dense_kernel(const int* rowptr, const unsigned* slot_of, const unsigned* dense, int n,
+                                            const long long* code_off, T* scode) {
+  const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int b = rowptr[r], e = rowptr[r + 1];
+  const long long cb = code_off[r >> 5];
+  const long long wp = (code_off[(r >> 5) + 1] - cb) >> 5;
+  const long long base = cb + (r & 31) * wp;
+  for (int k = 0; k < e - b; ++k) scode[base + k] = static_cast<T>(dense[slot_of[b + k]]);
+}
+
+// Builds the coded store of `op` from the staged CSR; leaves op plain when the operator has more
+// than 65535 distinct pairs. Returns a CUDA error only for real failures.
+static cudaError_t build_coded_store(qsg_op* op, const int* rp, const int* col, const double2* val, long long n,
+                                     const std::vector<long long>& w, cudaStream_t s) {
+  const long long nsl = static_cast<long long>(w.size());
+  cudaError_t e;
+  DevBuf tsig, toff, tval, ready, slot_of, dense, cnt, ovf, doff, dval;
+  if ((e = tsig.alloc(sizeof(unsigned long long) * kDictSlots, s)) || (e = toff.alloc(sizeof(int) * kDictSlots, s)) ||
+      (e = tval.alloc(sizeof(double2) * kDictSlots, s)) || (e = ready.alloc(sizeof(int) * kDictSlots, s)) ||
+      (e = slot_of.alloc(sizeof(unsigned) * op->nnz, s)) || (e = dense.alloc(sizeof(unsigned) * kDictSlots, s)) ||
+      (e = cnt.alloc(sizeof(int), s)) || (e = ovf.alloc(sizeof(int), s)) ||
+      (e = doff.alloc(sizeof(int) * 65536, s)) || (e = dval.alloc(sizeof(double2) * 65536, s)))
+    return e;
+  cudaMemsetAsync(tsig.p, 0, sizeof(unsigned long long) * kDictSlots, s);
+  cudaMemsetAsync(ready.p, 0, sizeof(int) * kDictSlots, s);
+  cudaMemsetAsync(ovf.p, 0, sizeof(int), s);
+  const unsigned nb = static_cast<unsigned>((n + 255) / 256);
+  dict_insert_kernel<<<nb, 256, 0, s>>>(rp, col, val, static_cast<int>(n), tsig.as<unsigned long long>(),
+                                        toff.as<int>(), tval.as<double2>(), ready.as<int>(), slot_of.as<unsigned>(),
+                                        ovf.as<int>());
+  dict_compact_kernel<<<1, 1024, 0, s>>>(tsig.as<unsigned long long>(), toff.as<int>(), tval.as<double2>(),
+                                         dense.as<unsigned>(), doff.as<int>(), dval.as<double2>(), 65536,
+                                         cnt.as<int>());
+  int count = 0, overflow = 0;
+  if ((e = cudaGetLastError()) || (e = cudaMemcpyAsync(&count, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+      (e = cudaMemcpyAsync(&overflow, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, s)) || (e = cudaStreamSynchronize(s)))
+    return e;
+  if (overflow || count < 1 || count > 65535) return cudaSuccess;  // stays plain
+  const int cbytes = count <= 256 ? 1 : 2;
+  std::vector<long long> coff(nsl + 1, 0);
+  for (long long i = 0; i < nsl; ++i) coff[i + 1] = coff[i] + 32 * ((w[i] + 7) / 8 * 8);
+  const size_t pc = static_cast<size_t>(std::max<long long>(1, coff[nsl]));
+  if ((e = cudaMalloc(&op->code, pc * cbytes)) || (e = cudaMalloc(&op->code_off, sizeof(long long) * (nsl + 1))) ||
+      (e = cudaMalloc(&op->dict_off, sizeof(int) * count)) || (e = cudaMalloc(&op->dict_val, sizeof(double2) * count)))
+    return e;
+  cudaMemsetAsync(op->code, 0, pc * cbytes, s);
+  cudaMemcpyAsync(op->code_off, coff.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(op->dict_off, doff.p, sizeof(int) * count, cudaMemcpyDeviceToDevice, s);
+  cudaMemcpyAsync(op->dict_val, dval.p, sizeof(double2) * count, cudaMemcpyDeviceToDevice, s);
+  if (cbytes == 1)
+    sell_code_fill_dense_kernel<unsigned char><<<nb, 256, 0, s>>>(rp, slot_of.as<unsigned>(), dense.as<unsigned>(),
+                                                                  static_cast<int>(n), op->code_off,
+                                                                  static_cast<unsigned char*>(op->code));
+  else
+    sell_code_fill_dense_kernel<unsigned short><<<nb, 256, 0, s>>>(rp, slot_of.as<unsigned>(), dense.as<unsigned>(),
+                                                                   static_cast<int>(n), op->code_off,
+                                                                   static_cast<unsigned short*>(op->code));
+  if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(s))) return e;
+  op->code_bytes = cbytes;
+  op->dict_n = count;
+  return cudaSuccess;
 }
 
 // ---- RNG kernel (rng.cpp:14-47) ---------------------------------------------------------------
@@ -612,52 +705,17 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
     qsg_op_destroy(op);
     return cuda_fail(e, "operator store build");
   }
-  // dictionary-coded store when the operator has few distinct (diagonal offset, value) pairs
+  // Dictionary-coded store when the operator streams from HBM (otherwise it is L2-resident and
+  // the code -> dictionary indirection only adds latency) and has <= 65535 distinct
+  // (diagonal offset, value) pairs. The plain entries stay resident too: the batched engine
+  // reads them. QSG_NO_COMPRESS=1 disables, QSG_COMPRESS_MIN_BYTES moves the size threshold.
   const char* nc = std::getenv("QSG_NO_COMPRESS");
-  if (!(nc && nc[0] == '1') && a->nnz > 0 && !is_device_ptr(a->col) && !is_device_ptr(a->val) &&
-      !is_device_ptr(a->rowptr)) {
-    PairDict pd = build_pair_dict(a);
-    if (pd.ok) {
-      const int cb = pd.off.size() <= 256 ? 1 : 2;
-      DevBuf d_codes;
-      std::vector<unsigned char> c8;
-      const void* src = pd.code.data();
-      if (cb == 1) {
-        c8.assign(pd.code.begin(), pd.code.end());
-        src = c8.data();
-      }
-      const size_t cbytes = static_cast<size_t>(a->nnz) * cb;
-      std::vector<long long> coff(nsl + 1, 0);
-      for (long long i = 0; i < nsl; ++i) coff[i + 1] = coff[i] + 32 * ((w[i] + 7) / 8 * 8);
-      const size_t pc = static_cast<size_t>(std::max<long long>(1, coff[nsl]));
-      if ((e = upload(d_codes, src, cbytes, s)) || (e = cudaMalloc(&op->code, pc * cb)) ||
-          (e = cudaMalloc(&op->code_off, sizeof(long long) * (nsl + 1))) ||
-          (e = cudaMalloc(&op->dict_off, sizeof(int) * pd.off.size())) ||
-          (e = cudaMalloc(&op->dict_val, sizeof(double2) * pd.val.size()))) {
-        qsg_op_destroy(op);
-        return cuda_fail(e, "coded operator store");
-      }
-      cudaMemsetAsync(op->code, 0, pc * cb, s);
-      cudaMemcpyAsync(op->code_off, coff.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, s);
-      cudaMemcpyAsync(op->dict_off, pd.off.data(), sizeof(int) * pd.off.size(), cudaMemcpyHostToDevice, s);
-      cudaMemcpyAsync(op->dict_val, pd.val.data(), sizeof(double2) * pd.val.size(), cudaMemcpyHostToDevice, s);
-      const unsigned nb = static_cast<unsigned>((n + 255) / 256);
-      if (cb == 1)
-        sell_code_fill_kernel<unsigned char><<<nb, 256, 0, s>>>(d_rp.as<int>(), d_codes.as<unsigned char>(),
-                                                                static_cast<int>(n), op->code_off,
-                                                                static_cast<unsigned char*>(op->code));
-      else
-        sell_code_fill_kernel<unsigned short><<<nb, 256, 0, s>>>(d_rp.as<int>(), d_codes.as<unsigned short>(),
-                                                                 static_cast<int>(n), op->code_off,
-                                                                 static_cast<unsigned short*>(op->code));
-      if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(s))) {
-        qsg_op_destroy(op);
-        return cuda_fail(e, "coded operator store build");
-      }
-      op->code_bytes = cb;
-      op->dict_n = static_cast<int>(pd.off.size());
-      // the plain entries stay resident too: the batched engine reads them (its operator is
-      // L2-resident, where the code -> dictionary indirection only adds latency)
+  long long min_bytes = 32LL << 20;
+  if (const char* mb = std::getenv("QSG_COMPRESS_MIN_BYTES")) min_bytes = std::atoll(mb);
+  if (!(nc && nc[0] == '1') && a->nnz > 0 && 20 * a->nnz >= min_bytes) {
+    if ((e = build_coded_store(op, d_rp.as<int>(), d_col.as<int>(), d_val.as<double2>(), n, w, s))) {
+      qsg_op_destroy(op);
+      return cuda_fail(e, "coded operator store");
     }
   }
   *out = op;

@@ -142,6 +142,7 @@ def test_invalid_tlist(ctx):
 def test_operator_store_formats_agree(ctx, monkeypatch, compress):
     """Plain and dictionary-coded SELL stores give the same SpMV and the same solve."""
     monkeypatch.setenv("QSG_NO_COMPRESS", "0" if compress == "1" else "1")
+    monkeypatch.setenv("QSG_COMPRESS_MIN_BYTES", "0")  # code even this L2-sized operator
     m = O.Model("ising", 3, 2, 1.0, 0.2, 1.0, 1)
     gen = oracle_generator(ctx, m, "me")
     cb, nd = q.op_storage(gen.ops[0])
