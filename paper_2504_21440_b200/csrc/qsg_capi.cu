@@ -546,7 +546,9 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "occupancy");
   const int max_grid = per_sm * ctx->sm_count;
   const long long nblk = (n + 31) / 32;
-  int grid = static_cast<int>(std::min<long long>(max_grid, std::max<long long>(1, (n + 2047) / 2048)));
+  // ~4 slices (128 rows) per CTA: small systems are latency-bound and gain from spreading out
+  // (Kerr N=200: 60 -> 30 us per attempt from 20 to 148 CTAs, profiles/r01_summary.md)
+  int grid = static_cast<int>(std::min<long long>(max_grid, std::max<long long>(1, (nblk + 3) / 4)));
   if (const char* eg = std::getenv("QSG_GRID")) grid = std::max(1, std::min(max_grid, std::atoi(eg)));
   grid = static_cast<int>(std::min<long long>(grid, nblk));
   (void)threads;
