@@ -1,0 +1,85 @@
+"""GPU parity at the BASELINE sizes (configs[1] and configs[2]), through the product's own model
+builder and operator store (dictionary-coded for TFIM-10), against the CPU oracle.
+
+Full solves at these sizes take the oracle ~50 s (TFIM-10) and ~1 s per trajectory (TFIM-14), so
+the deterministic check runs the first 0.5 time units of the TFIM-10 solve (13 DP5 attempts) and
+the first 16 trajectories of the 14-spin ensemble; the full-length solves are checked through
+size-independent properties (trace, hermiticity of the observables, monotone jump records).
+"""
+import numpy as np
+import pytest
+
+import paper_2504_21440_b200 as q
+from oracle import oracle as O
+from tests._helpers import assert_stats_close, normwise_rel
+
+pytestmark = pytest.mark.gpu
+
+TFIM10 = (10, 1, 1.0, 0.2, 1.0, 1)
+TFIM14 = (14, 1, 1.0, 0.2, 1.0, 1)
+
+
+@pytest.fixture(scope="module")
+def tfim10(ctx):
+    m = q.Model("ising", *TFIM10)
+    L = m.export(q.SEL_L_CONST)
+    op = ctx.op(L)
+    eops = [m.export(q.SEL_E_OP, k) for k in range(m.n_eops)]
+    psi = m.psi0()
+    rho0 = np.outer(psi, psi.conj()).reshape(-1, order="F").copy()
+    return m, op, eops, rho0
+
+
+def test_tfim10_store_is_coded(tfim10):
+    _, op, _, _ = tfim10
+    assert q.op_storage(op) == (1, 201)
+
+
+def test_tfim10_mesolve_prefix_matches_oracle(ctx, tfim10):
+    m, op, eops, rho0 = tfim10
+    t = np.linspace(0.0, 0.5, 6)
+    dev = q.mesolve(ctx, q.Generator([op]), m.dim, rho0, t, eops)
+    om = O.Model("ising", *TFIM10)
+    om.prepare_liouvillian()
+    ex, st = om.mesolve_prepared(t)
+    assert normwise_rel(dev["expect"], ex) <= 1e-6
+    assert_stats_close(dev["stats"], st)
+
+
+def test_tfim10_full_solve_properties(ctx, tfim10):
+    """Full configs[1] solve: trace preservation shows up as Sz_total staying in [-10, 10] and
+    the observables being real (hermitized trace formula, evolve.cpp:286-295)."""
+    m, op, eops, rho0 = tfim10
+    t = np.linspace(0.0, 10.0, 100)
+    r = q.mesolve(ctx, q.Generator([op]), m.dim, rho0, t, eops)
+    ex = r["expect"]
+    assert r["stats"][2] == 2 + 6 * (r["stats"][0] + r["stats"][1])
+    assert np.max(np.abs(ex.imag)) < 1e-10
+    assert abs(ex[2, 0].real - 10.0) < 1e-12  # all spins up at t = 0
+    assert np.all(np.abs(ex.real) <= 10.0 + 1e-9)
+    assert ex[2, -1].real < ex[2, 0].real  # decay towards the steady state
+
+
+def test_tfim14_first_trajectories_match_oracle(ctx):
+    """configs[2]: trajectories 0..15 of seed 2025 (RngStream(2025, i)), per trajectory."""
+    m = q.Model("ising", *TFIM14)
+    G = q.Generator([ctx.op(m.export(q.SEL_MC_GEN))])
+    cops = [m.export(q.SEL_C_OP, k) for k in range(m.n_cops)]
+    eops = [m.export(q.SEL_E_OP, 2)]
+    t = np.linspace(0.0, 10.0, 100)
+    dev = q.mcsolve(ctx, G, cops, eops, m.dim, m.psi0(), t, 2025, 0, 16)
+    om = O.Model("ising", *TFIM14)
+    ref = om.mcsolve(t, 2025, 16)
+    diverged = 0
+    for i in range(16):
+        dj, rj = dev["jumps"][i], ref["jumps"][i]
+        same = len(dj) == len(rj) and all(a[1] == b[1] and abs(a[0] - b[0]) <= 1e-6 for a, b in zip(dj, rj))
+        if not same:
+            diverged += 1
+            continue
+        # Sz_total expectations of trajectory i (oracle e_ops are Sx, Sy, Sz: take index 2)
+        assert normwise_rel(dev["per_traj"][i][0], ref["per_traj"][i][2]) <= 1e-6, i
+    assert diverged <= 1, diverged
+    for i in range(16):
+        times = [j[0] for j in dev["jumps"][i]]
+        assert all(b > a for a, b in zip(times, times[1:]))
