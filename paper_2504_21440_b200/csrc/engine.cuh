@@ -263,7 +263,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int G) {
       __threadfence();
       st_release_gpu(bar + 1, gen + 1);
     } else {
-      while (ld_acquire_gpu(bar + 1) == gen) __nanosleep(20);
+      while (ld_acquire_gpu(bar + 1) == gen) {
+      }
     }
     __threadfence();
   }
