@@ -118,6 +118,8 @@ qsg_status qsg_device_info(qsg_ctx* ctx, int* sm_count, int64_t* l2_bytes, char*
 
 /* Upload a CSR operator into HBM (evolve.cpp:53-61 materialises P*A once per solve). */
 qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out);
+/* Frees the store stream-ordered on its context's stream. A context stays alive until its last
+ * operator is destroyed, so the two may be destroyed in either order. */
 void qsg_op_destroy(qsg_op* op);
 int64_t qsg_op_nnz(const qsg_op* op);
 int64_t qsg_op_rows(const qsg_op* op);

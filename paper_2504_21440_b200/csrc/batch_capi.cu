@@ -51,6 +51,7 @@ struct RunOut {
   long long attempts = 0;
   int grid = 0;
   bool grid_mode = false;
+  int layout = 0;
 };
 
 // Runs systems [sys_begin, sys_begin + n_sys) through the batch kernel and downloads outputs.
@@ -59,29 +60,46 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   cudaError_t ce;
   P.n_systems = n_sys;
   P.jump_cap = jump_cap;
-  // grid mode keeps one 32-slot batch L2-resident across the whole GPU; it needs enough rows
-  // per CTA to be worth the grid barriers. QSG_BATCH_MODE=grid|local overrides.
-  // Measured on TFIM-14 (profiles/r01_summary.md): the grid batch wins while per-CTA batches
-  // would leave the GPU half empty (64 trajectories: 0.20 s vs 2.9 s); for large ensembles the
-  // per-CTA batches stream more work per barrier (2368 trajectories: 484 vs 312 traj/s).
-  const size_t grid_ws = batch_work_stride(P.n, true) * sizeof(double2);
-  const long long local_slots = static_cast<long long>(batch_max_blocks_per_sm(false)) * ctx->sm_count * batch_slots(false);
-  bool grid_mode = P.n >= 4096 && grid_ws <= static_cast<size_t>(ctx->l2_bytes) * 85 / 100 &&
-                   n_sys < local_slots * 5 / 8;
-  if (const char* m = std::getenv("QSG_BATCH_MODE")) grid_mode = std::string(m) == "grid";
-  const int per_sm = batch_max_blocks_per_sm(grid_mode);
+  // Layouts (batch_engine.cu): 4 = one trajectory per CTA (default), 1 = one 32-slot batch spread
+  // over the whole GPU, 0/2/3 = 8/4/2 slots per CTA (kept for measurement).
+  // Measured on TFIM-14 (profiles/r01_summary.md, scripts/probe_mcmodes.py): one trajectory per
+  // CTA wins from ~300 trajectories up (740 traj/s at 10,000 vs 621/500/428 for 2/4/8 slots and
+  // 274 for the grid batch): its private state is smallest, so more of it stays in L1/L2. The grid
+  // batch wins only while per-CTA runs would leave most SMs idle (64 trajectories: 330 vs 296).
+  // QSG_BATCH_MODE=grid|local|local4|local2|local1 overrides.
+  const long long slots1 = static_cast<long long>(batch_max_blocks_per_sm(4)) * ctx->sm_count;
+  int layout = 4;
+  if (P.n >= 4096 && n_sys * 3 < slots1) layout = 1;
+  if (const char* m = std::getenv("QSG_BATCH_MODE")) {
+    const std::string v(m);
+    layout = v == "grid" ? 1 : v == "local" ? 0 : v == "local4" ? 2 : v == "local2" ? 3 : 4;
+  }
+  const bool grid_mode = layout == 1;
+  const int per_sm = batch_max_blocks_per_sm(layout);
   if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "batch occupancy");
   int grid;
   if (grid_mode) {
     grid = std::min(per_sm * ctx->sm_count, (P.n + 31) / 32);
   } else {
-    const long long want = (n_sys + batch_slots(false) - 1) / batch_slots(false);
+    const long long want = (n_sys + batch_slots(layout) - 1) / batch_slots(layout);
     grid = static_cast<int>(std::min<long long>(static_cast<long long>(per_sm) * ctx->sm_count, want));
   }
   if (const char* eg = std::getenv("QSG_BATCH_GRID")) grid = std::max(1, std::min(grid, std::atoi(eg)));
+  const size_t stride = batch_work_stride(P.n, layout);
+  if (!grid_mode) {  // per-CTA workspaces: fit them in 60% of free memory (the queue refills CTAs)
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+      const long long fit = static_cast<long long>(fr / 10 * 6 / (stride * sizeof(double2)));
+      if (fit < 1) {
+        set_error("OutOfMemory: batch workspace does not fit on the device");
+        return QSG_OUT_OF_MEMORY;
+      }
+      grid = static_cast<int>(std::min<long long>(grid, fit));
+    }
+  }
   o.grid = grid;
   o.grid_mode = grid_mode;
-  const size_t stride = batch_work_stride(P.n, grid_mode);
+  o.layout = layout;
   DevBuf work, q, ex, st, ft, stt, jc, jt, jch, att, gp, gf, gb;
   const size_t nvals = static_cast<size_t>(std::max(1, P.n_e)) * P.n_t;
   if ((ce = work.alloc(stride * (grid_mode ? 1 : grid) * sizeof(double2), s)) || (ce = q.alloc(8, s)) ||
@@ -113,7 +131,7 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   P.gfin = gf.as<double>();
   P.bar = gb.as<unsigned>();
   cudaEventRecord(ctx->ev[2], s);
-  if ((ce = launch_batch(P, grid_mode, grid, s))) return cuda_fail(ce, "batch launch");
+  if ((ce = launch_batch(P, layout, grid, s))) return cuda_fail(ce, "batch launch");
   cudaEventRecord(ctx->ev[3], s);
   o.expect.resize(nvals * n_sys);
   o.status.resize(n_sys);
@@ -259,7 +277,7 @@ extern "C" qsg_status qsg_mcsolve(qsg_ctx* ctx, const qsg_generator* G, int32_t 
     timing->kernel_ms = o.kernel_ms;
     timing->attempts = o.attempts;
     timing->grid_ctas = o.grid;
-    timing->lanes = batch_slots(o.grid_mode);
+    timing->lanes = batch_slots(o.layout);
   }
   return QSG_OK;
 }
@@ -335,7 +353,7 @@ extern "C" qsg_status qsg_mesolve_batch(qsg_ctx* ctx, const qsg_generator* L, in
     timing->kernel_ms = o.kernel_ms;
     timing->attempts = o.attempts;
     timing->grid_ctas = o.grid;
-    timing->lanes = batch_slots(o.grid_mode);
+    timing->lanes = batch_slots(o.layout);
   }
   return status ? QSG_OK : rc;
 }

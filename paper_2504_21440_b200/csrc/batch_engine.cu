@@ -852,23 +852,40 @@ int occupancy_of() {
 
 }  // namespace
 
-int batch_slots(bool grid) { return grid ? kMaxB : 8; }
+// layouts: 0 = per-CTA batches of 8 slots, 1 = grid-wide batch of 32 slots, 2 = per-CTA batches of
+// 4 slots (fills the GPU with half as many trajectories as layout 0)
+int batch_slots(int layout) { return layout == 1 ? kMaxB : layout == 2 ? 4 : layout == 3 ? 2 : layout == 4 ? 1 : 8; }
 
-size_t batch_work_stride(int n, bool grid) {
-  return static_cast<size_t>(NBUF) * static_cast<size_t>(n) * batch_slots(grid);
+size_t batch_work_stride(int n, int layout) {
+  return static_cast<size_t>(NBUF) * static_cast<size_t>(n) * batch_slots(layout);
 }
 
-int batch_max_blocks_per_sm(bool grid) { return grid ? occupancy_of<kMaxB, true>() : occupancy_of<8, false>(); }
+int batch_max_blocks_per_sm(int layout) {
+  return layout == 1 ? occupancy_of<kMaxB, true>() : layout == 2 ? occupancy_of<4, false>()
+         : layout == 3 ? occupancy_of<2, false>() : layout == 4 ? occupancy_of<1, false>()
+         : occupancy_of<8, false>();
+}
 
-cudaError_t launch_batch(const BatchProblem& P, bool grid_mode, int grid, cudaStream_t s) {
-  if (grid_mode) {
+cudaError_t launch_batch(const BatchProblem& P, int layout, int grid, cudaStream_t s) {
+  if (layout == 1) {
     void* args[] = {const_cast<BatchProblem*>(&P)};
     set_attrs<kMaxB, true>();
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(batch_kernel<kMaxB, true>), dim3(grid),
                                        dim3(kThreads), args, dyn_smem<kMaxB, true>(), s);
   }
-  set_attrs<8, false>();
-  batch_kernel<8, false><<<grid, kThreads, dyn_smem<8, false>(), s>>>(P);
+  if (layout == 2) {
+    set_attrs<4, false>();
+    batch_kernel<4, false><<<grid, kThreads, dyn_smem<4, false>(), s>>>(P);
+  } else if (layout == 4) {
+    set_attrs<1, false>();
+    batch_kernel<1, false><<<grid, kThreads, dyn_smem<1, false>(), s>>>(P);
+  } else if (layout == 3) {
+    set_attrs<2, false>();
+    batch_kernel<2, false><<<grid, kThreads, dyn_smem<2, false>(), s>>>(P);
+  } else {
+    set_attrs<8, false>();
+    batch_kernel<8, false><<<grid, kThreads, dyn_smem<8, false>(), s>>>(P);
+  }
   return cudaGetLastError();
 }
 

@@ -57,9 +57,9 @@ struct BatchProblem {
   unsigned* bar;  // {count, generation}
 };
 
-int batch_slots(bool grid);
-cudaError_t launch_batch(const BatchProblem& P, bool grid_mode, int grid, cudaStream_t s);
-int batch_max_blocks_per_sm(bool grid);
-size_t batch_work_stride(int n, bool grid);  // double2 elements per batch
+int batch_slots(int layout);
+cudaError_t launch_batch(const BatchProblem& P, int layout, int grid, cudaStream_t s);
+int batch_max_blocks_per_sm(int layout);
+size_t batch_work_stride(int n, int layout);  // double2 elements per batch
 
 }  // namespace qsg

@@ -2,6 +2,7 @@
 // Reference seams replaced are cited per entry point in include/qsg.h.
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -351,8 +352,10 @@ static cudaError_t build_coded_store(qsg_op* op, const int* rp, const int* col, 
   std::vector<long long> coff(nsl + 1, 0);
   for (long long i = 0; i < nsl; ++i) coff[i + 1] = coff[i] + 32 * ((w[i] + 7) / 8 * 8);
   const size_t pc = static_cast<size_t>(std::max<long long>(1, coff[nsl]));
-  if ((e = cudaMalloc(&op->code, pc * cbytes)) || (e = cudaMalloc(&op->code_off, sizeof(long long) * (nsl + 1))) ||
-      (e = cudaMalloc(&op->dict_off, sizeof(int) * count)) || (e = cudaMalloc(&op->dict_val, sizeof(double2) * count)))
+  if ((e = cudaMallocAsync(&op->code, pc * cbytes, s)) ||
+      (e = cudaMallocAsync(&op->code_off, sizeof(long long) * (nsl + 1), s)) ||
+      (e = cudaMallocAsync(&op->dict_off, sizeof(int) * count, s)) ||
+      (e = cudaMallocAsync(&op->dict_val, sizeof(double2) * count, s)))
     return e;
   cudaMemsetAsync(op->code, 0, pc * cbytes, s);
   cudaMemcpyAsync(op->code_off, coff.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, s);
@@ -626,18 +629,30 @@ qsg_status qsg_ctx_create(int device, qsg_ctx** out) {
     return cuda_fail(e, "stream");
   }
   for (auto& ev : c->ev) cudaEventCreate(&ev);
+  // All device memory of the library (operator stores, solver workspaces) comes from the device's
+  // stream-ordered pool. Keep freed blocks reserved instead of returning them to the driver at
+  // every synchronisation: repeated op_create/solve/destroy cycles then cost no remapping.
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    unsigned long long thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
   *out = c;
   return QSG_OK;
 }
 
-void qsg_ctx_destroy(qsg_ctx* ctx) {
-  if (!ctx) return;
+static void ctx_release(qsg_ctx* ctx) {
+  if (ctx->refs.fetch_sub(1) != 1) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (auto& ev : ctx->ev) cudaEventDestroy(ev);
   if (ctx->work) cudaFree(ctx->work);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
+}
+
+void qsg_ctx_destroy(qsg_ctx* ctx) {
+  if (ctx) ctx_release(ctx);
 }
 
 qsg_status qsg_device_info(qsg_ctx* ctx, int* sm_count, int64_t* l2_bytes, char* name, int name_len) {
@@ -662,6 +677,15 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
   cudaStream_t s = ctx->stream;
   const long long n = a->n_rows, nsl = (n + 31) / 32;
   cudaError_t e;
+  static const bool trace = std::getenv("QSG_TRACE_OP") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[qsg op] %-10s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   // stage the CSR in HBM
   DevBuf d_rp, d_col, d_val, d_w;
   if ((e = upload(d_rp, a->rowptr, sizeof(int) * (n + 1), s)) ||
@@ -669,14 +693,16 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
       (e = upload(d_val, a->val, sizeof(double2) * a->nnz, s)) ||
       (e = d_w.alloc(sizeof(long long) * nsl, s)))
     return cuda_fail(e, "operator staging");
+  mark("upload");
   auto* op = new qsg_op;
   op->ctx = ctx;
+  ctx->refs.fetch_add(1);
   op->n_rows = n;
   op->n_cols = a->n_cols;
   op->nnz = a->nnz;
   op->n_slices = nsl;
-  if ((e = cudaMalloc(&op->rowlen, sizeof(int) * nsl * 32)) ||
-      (e = cudaMalloc(&op->slice_off, sizeof(long long) * (nsl + 1)))) {
+  if ((e = cudaMallocAsync(&op->rowlen, sizeof(int) * nsl * 32, s)) ||
+      (e = cudaMallocAsync(&op->slice_off, sizeof(long long) * (nsl + 1), s))) {
     qsg_op_destroy(op);
     return cuda_fail(e, "operator store allocation");
   }
@@ -688,25 +714,30 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
     qsg_op_destroy(op);
     return cuda_fail(e, "operator widths");
   }
+  mark("widths");
   for (long long i = 0; i < nsl; ++i) {
     off[i + 1] = off[i] + w[i];
     op->max_rowlen = std::max<int>(op->max_rowlen, static_cast<int>(w[i]));
   }
   op->padded_cols = off[nsl];
   const size_t pe = static_cast<size_t>(std::max<long long>(1, off[nsl] * 32));
-  if ((e = cudaMalloc(&op->col, sizeof(int) * pe)) || (e = cudaMalloc(&op->val, sizeof(double2) * pe))) {
+  if ((e = cudaMallocAsync(&op->col, sizeof(int) * pe, s)) || (e = cudaMallocAsync(&op->val, sizeof(double2) * pe, s))) {
     qsg_op_destroy(op);
     return cuda_fail(e, "operator store allocation");
   }
+  mark("alloc");
   cudaMemsetAsync(op->col, 0, sizeof(int) * pe, s);
   cudaMemsetAsync(op->val, 0, sizeof(double2) * pe, s);
+  mark("memset");
   cudaMemcpyAsync(op->slice_off, off.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, s);
+  mark("slice_off");
   sell_fill_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
       d_rp.as<int>(), d_col.as<int>(), d_val.as<double2>(), static_cast<int>(n), op->slice_off, op->col, op->val);
   if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(s))) {
     qsg_op_destroy(op);
     return cuda_fail(e, "operator store build");
   }
+  mark("sell fill");
   // Dictionary-coded store when the operator streams from HBM (otherwise it is L2-resident and
   // the code -> dictionary indirection only adds latency) and has <= 65535 distinct
   // (diagonal offset, value) pairs. The plain entries stay resident too: the batched engine
@@ -719,6 +750,7 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
       qsg_op_destroy(op);
       return cuda_fail(e, "coded operator store");
     }
+    mark("coded");
   }
   *out = op;
   return QSG_OK;
@@ -726,15 +758,17 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
 
 void qsg_op_destroy(qsg_op* op) {
   if (!op) return;
-  cudaFree(op->code);
-  cudaFree(op->code_off);
-  cudaFree(op->dict_off);
-  cudaFree(op->dict_val);
-  cudaFree(op->slice_off);
-  cudaFree(op->rowlen);
-  cudaFree(op->col);
-  cudaFree(op->val);
+  // stream-ordered frees back into the context's pool: later solves on the same stream reuse the
+  // memory without a device synchronisation or an unmap
+  cudaSetDevice(op->ctx->device);
+  cudaStream_t s = op->ctx->stream;
+  for (void* p : {op->code, static_cast<void*>(op->code_off), static_cast<void*>(op->dict_off),
+                  static_cast<void*>(op->dict_val), static_cast<void*>(op->slice_off),
+                  static_cast<void*>(op->rowlen), static_cast<void*>(op->col), static_cast<void*>(op->val)})
+    if (p) cudaFreeAsync(p, s);
+  qsg_ctx* ctx = op->ctx;
   delete op;
+  ctx_release(ctx);
 }
 
 int64_t qsg_op_nnz(const qsg_op* op) { return op ? op->nnz : 0; }

@@ -1,6 +1,7 @@
 // Internal host-side structures shared by the C-ABI translation units.
 #pragma once
 
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -19,6 +20,9 @@ struct qsg_ctx {
   // cached solver workspace
   void* work = nullptr;
   size_t work_bytes = 0;
+  // lifetime: one reference held by the creator (dropped by qsg_ctx_destroy) plus one per live
+  // operator, so an operator destroyed after its context can still free on the context's stream
+  std::atomic<int> refs{1};
 };
 
 // HBM operator store: SELL-32 layout (engine.cuh DevSell) built on device from the CSR input.

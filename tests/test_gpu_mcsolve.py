@@ -127,9 +127,12 @@ def test_mesolve_batch_sweep_parity(ctx):
         assert_stats_close(res["stats"][p], st)
 
 
-@pytest.fixture(params=["local", "grid"])
+MODES = ["local1", "local2", "local4", "local", "grid"]
+
+
+@pytest.fixture(params=MODES)
 def batch_mode(request, monkeypatch):
-    """Both batch-engine layouts: per-CTA batches and the grid-wide L2-resident batch."""
+    """Every batch-engine layout: 1/2/4/8 slots per CTA and the grid-wide 32-slot batch."""
     monkeypatch.setenv("QSG_BATCH_MODE", request.param)
     return request.param
 
@@ -151,15 +154,16 @@ def test_both_modes_threshold_crossing(ctx, batch_mode):
 
 
 def test_both_modes_ising_identical(ctx, monkeypatch):
-    """Grid-wide and per-CTA batches give the same per-trajectory records (TFIM-7 chain)."""
+    """All layouts give the same per-trajectory records (TFIM-7 chain)."""
     m = O.Model("ising", 7, 1, 1.0, 0.2, 1.0, 1)
     t = np.linspace(0, 10, 100)
     out = {}
-    for mode in ("local", "grid"):
+    for mode in MODES:
         monkeypatch.setenv("QSG_BATCH_MODE", mode)
         out[mode] = _mc(ctx, m, t, 2025, 0, 40)
     # same trajectories; only the reduction order differs (jump times agree to ~1e-13)
-    _compare_trajectories(out["grid"], out["local"], jt_tol=1e-9, ex_tol=1e-9, allow_diverged=1)
+    for mode in MODES[1:]:
+        _compare_trajectories(out[mode], out["local1"], jt_tol=1e-9, ex_tol=1e-9, allow_diverged=1)
     ref = m.mcsolve(t, 2025, 40)
     _compare_trajectories(out["grid"], ref, allow_diverged=1)
 

@@ -156,3 +156,17 @@ def test_operator_store_formats_agree(ctx, monkeypatch, compress):
     res = q.mesolve(ctx, gen, m.dim, rho0_vec(m), t, e_ops_csr(m))
     ex, st, _ = m.mesolve(t)
     assert normwise_rel(res["expect"], ex) <= TOL
+
+
+def test_context_outlives_its_operators():
+    """qsg_ctx_destroy before qsg_op_destroy: the context is released by its last operator."""
+    c = q.Context(0)
+    m = O.Model("kerr", 6, 1.0, 0.1, 0.5, 0.5)
+    a = c.op(csr_from_oracle(m, O.L_CONST))
+    b = c.op(csr_from_oracle(m, O.L_CONST))
+    y = np.ones(a.n, complex)
+    ref = q.generator_apply(c, q.Generator([a]), y)
+    c.close()  # drops the creator's reference; the two operators still pin the context
+    a.close()
+    b.close()  # last reference: frees the store, then the context
+    assert np.all(np.isfinite(ref))
