@@ -93,14 +93,17 @@ __device__ double rng_uniform_pos(unsigned long long* s) {
   return u;
 }
 
+// Logical buffer k of slot s lives in physical array map[s][k]: an accepted step relabels
+// (Y, YO, Y1) and (K1, K1O, K7) instead of copying them (FSAL, integrator.hpp:135-137).
 template <int BS>
 struct Ctx {
   const BatchProblem& P;
   double2* w;  // batch workspace: NBUF arrays of [n][BS]
   int n;
-  __device__ double2* buf(int k) const { return w + static_cast<long long>(k) * n * BS; }
-  __device__ double2 ld(int k, int r, int s) const { return buf(k)[static_cast<long long>(r) * BS + s]; }
-  __device__ void st(int k, int r, int s, double2 v) const { buf(k)[static_cast<long long>(r) * BS + s] = v; }
+  const unsigned char (*map)[NBUF];  // shared memory, per slot
+  __device__ double2* buf(int k, int s) const { return w + static_cast<long long>(map[s][k]) * n * BS; }
+  __device__ double2 ld(int k, int r, int s) const { return buf(k, s)[static_cast<long long>(r) * BS + s]; }
+  __device__ void st(int k, int r, int s, double2 v) const { buf(k, s)[static_cast<long long>(r) * BS + s] = v; }
 };
 
 // dense output of slot s at index c (integrator.hpp:127-131,150-154) from the committed step
@@ -109,7 +112,8 @@ __device__ __forceinline__ double2 dense_at(const Ctx<BS>& C, int c, int s, doub
   if (src == SRC_Y) return C.ld(Y, c, s);
   if (src == SRC_SC) return C.ld(SC, c, s);
   using namespace dp;
-  const double2 yo = C.ld(YO, c, s), y1 = C.ld(Y, c, s), k1 = C.ld(K1O, c, s), k7 = C.ld(K7, c, s);
+  // after the commit relabelling K1 holds the step's k7 (FSAL) and K1O its k1
+  const double2 yo = C.ld(YO, c, s), y1 = C.ld(Y, c, s), k1 = C.ld(K1O, c, s), k7 = C.ld(K1, c, s);
   const double2 k3 = C.ld(K3, c, s), k4 = C.ld(K4, c, s), k5 = C.ld(K5, c, s), k6 = C.ld(K6, c, s);
   const double th1 = 1.0 - theta;
   const double2 rc2 = csub(y1, yo);
@@ -276,11 +280,12 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
   __shared__ double sout[BS * 15];
   __shared__ int s_alldone;
   __shared__ long long s_next;
+  __shared__ unsigned char s_map[BS][NBUF];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sl = lane % B, rs = lane / B;
   const int n = P.n;
-  const Ctx<BS> C{P, P.work + (GRID ? 0LL : static_cast<long long>(blockIdx.x) * P.work_stride), n};
+  const Ctx<BS> C{P, P.work + (GRID ? 0LL : static_cast<long long>(blockIdx.x) * P.work_stride), n, s_map};
   const double atol = P.atol, rtol = P.rtol, eps_t = P.eps_t, tf = P.tf, t0 = P.t0;
   const bool out_cta = !GRID || blockIdx.x == 0;  // the CTA that writes per-system outputs
   const int rpc = GRID ? (n + gridDim.x - 1) / static_cast<int>(gridDim.x) : n;
@@ -318,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         else idx = atomicAdd(P.queue, 1ull);
         if (idx < static_cast<unsigned long long>(P.n_systems)) {
           s.sys = static_cast<long long>(idx);
+          for (int k = 0; k < NBUF; ++k) s_map[threadIdx.x][k] = static_cast<unsigned char>(k);
           s.phase = START;
           s.fresh = 1;
           s.status = kRunning;
@@ -732,12 +738,12 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       for (int a = 0; a < 15; ++a) g[a] = 0.0;
       const bool acc_ok = S[sl].phase == RUN && S[sl].accepted;
       const bool cross = acc_ok && S[sl].crossing;
-      if (acc_ok) {
+      if (cross) {
         const double h = S[sl].h_last;
         using namespace dp;
         rows([&](int r) {
           const double2 yo = C.ld(Y, r, sl), y1 = C.ld(Y1, r, sl), k1 = C.ld(K1, r, sl), k7 = C.ld(K7, r, sl);
-          if (cross) {
+          {
             const double2 k3 = C.ld(K3, r, sl), k4 = C.ld(K4, r, sl), k5 = C.ld(K5, r, sl), k6 = C.ld(K6, r, sl);
             double2 rc[5];
             rc[0] = yo;
@@ -752,10 +758,6 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
 #pragma unroll
               for (int b = a; b < 5; ++b) g[q++] += rc[a].x * rc[b].x + rc[a].y * rc[b].y;  // Re <rc_a, rc_b>
           }
-          C.st(K1O, r, sl, k1);
-          C.st(YO, r, sl, yo);
-          C.st(Y, r, sl, y1);
-          C.st(K1, r, sl, k7);
         });
       }
       bool anyc = false;
@@ -764,6 +766,15 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       else __syncthreads();
       if (threadIdx.x < B && S[threadIdx.x].phase == RUN && S[threadIdx.x].accepted) {
         Slot& s = S[threadIdx.x];
+        // commit by relabelling: YO <- Y, Y <- Y1, Y1 <- old YO; K1O <- K1, K1 <- K7, K7 <- old K1O
+        unsigned char* m = s_map[threadIdx.x];
+        const unsigned char y = m[Y], yo = m[YO], y1 = m[Y1], k1 = m[K1], k1o = m[K1O], k7 = m[K7];
+        m[YO] = y;
+        m[Y] = y1;
+        m[Y1] = yo;
+        m[K1O] = k1;
+        m[K1] = k7;
+        m[K7] = k1o;
         double jt = s.t;
         if (s.crossing) {
           for (int a = 0; a < 15; ++a) s.gram[a] = sout[threadIdx.x * 15 + a];
