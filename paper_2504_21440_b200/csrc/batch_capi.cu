@@ -21,11 +21,19 @@ struct TmpOps {
   }
 };
 
+// The batch engine reads the plain store unless QSG_BATCH_CODES=1: its operators are re-read by
+// every CTA from L2, and on TFIM-14 the code -> dictionary hop made the gathers slower
+// (705 vs 763 traj/s, profiles/r01_summary.md).
+bool batch_codes() {
+  const char* e = std::getenv("QSG_BATCH_CODES");
+  return e && e[0] == '1';
+}
+
 qsg_status make_sell(qsg_ctx* ctx, const qsg_csr& a, TmpOps& keep, DevSell& out) {
   qsg_op* op = nullptr;
   if (qsg_status s = qsg_op_create(ctx, &a, &op)) return s;
   keep.ops.push_back(op);
-  out = sell_view(op, false);
+  out = sell_view(op, batch_codes());
   return QSG_OK;
 }
 
@@ -61,32 +69,47 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   P.n_systems = n_sys;
   P.jump_cap = jump_cap;
   // Layouts (batch_engine.cu): 4 = one trajectory per CTA (default), 1 = one 32-slot batch spread
-  // over the whole GPU, 0/2/3 = 8/4/2 slots per CTA (kept for measurement).
+  // over the whole GPU, 0/2/3 = 8/4/2 slots per CTA, 5/6 = 1/2 slots per thread-block cluster.
   // Measured on TFIM-14 (profiles/r01_summary.md, scripts/probe_mcmodes.py): one trajectory per
-  // CTA wins from ~300 trajectories up (740 traj/s at 10,000 vs 621/500/428 for 2/4/8 slots and
-  // 274 for the grid batch): its private state is smallest, so more of it stays in L1/L2. The grid
-  // batch wins only while per-CTA runs would leave most SMs idle (64 trajectories: 330 vs 296).
-  // QSG_BATCH_MODE=grid|local|local4|local2|local1 overrides.
+  // CTA wins from ~300 trajectories up among the CTA layouts (740 traj/s at 10,000 vs 621/500/428
+  // for 2/4/8 slots and 274 for the grid batch): its private state is smallest, so more of it
+  // stays in L1/L2. The grid batch wins only while per-CTA runs would leave most SMs idle.
+  // QSG_BATCH_MODE=grid|local|local4|local2|local1|cluster1|cluster2 overrides;
+  // QSG_CLUSTER sets the cluster size (default 16).
   const long long slots1 = static_cast<long long>(batch_max_blocks_per_sm(4)) * ctx->sm_count;
   int layout = 4;
   if (P.n >= 4096 && n_sys * 3 < slots1) layout = 1;
   if (const char* m = std::getenv("QSG_BATCH_MODE")) {
     const std::string v(m);
-    layout = v == "grid" ? 1 : v == "local" ? 0 : v == "local4" ? 2 : v == "local2" ? 3 : 4;
+    layout = v == "grid"       ? 1
+             : v == "local"    ? 0
+             : v == "local4"   ? 2
+             : v == "local2"   ? 3
+             : v == "cluster1" ? 5
+             : v == "cluster2" ? 6
+                               : 4;
   }
+  int cs = 16;
+  if (const char* c = std::getenv("QSG_CLUSTER")) cs = std::max(1, std::min(16, std::atoi(c)));
   const bool grid_mode = layout == 1;
+  const bool cluster_mode = layout == 5 || layout == 6;
   const int per_sm = batch_max_blocks_per_sm(layout);
   if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "batch occupancy");
+  const long long want = (n_sys + batch_slots(layout) - 1) / batch_slots(layout);  // batches
   int grid;
   if (grid_mode) {
     grid = std::min(per_sm * ctx->sm_count, (P.n + 31) / 32);
+  } else if (cluster_mode) {
+    const int cap = batch_max_clusters(layout, cs);
+    if (cap <= 0) return cuda_fail(cudaGetLastError(), "cluster occupancy");
+    grid = static_cast<int>(std::min<long long>(cap, want)) * cs;
   } else {
-    const long long want = (n_sys + batch_slots(layout) - 1) / batch_slots(layout);
     grid = static_cast<int>(std::min<long long>(static_cast<long long>(per_sm) * ctx->sm_count, want));
   }
   if (const char* eg = std::getenv("QSG_BATCH_GRID")) grid = std::max(1, std::min(grid, std::atoi(eg)));
   const size_t stride = batch_work_stride(P.n, layout);
-  if (!grid_mode) {  // per-CTA workspaces: fit them in 60% of free memory (the queue refills CTAs)
+  const int n_batches = grid_mode ? 1 : cluster_mode ? grid / cs : grid;
+  if (!grid_mode) {  // per-batch workspaces: fit them in 60% of free memory (the queue refills)
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
       const long long fit = static_cast<long long>(fr / 10 * 6 / (stride * sizeof(double2)));
@@ -94,7 +117,7 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
         set_error("OutOfMemory: batch workspace does not fit on the device");
         return QSG_OUT_OF_MEMORY;
       }
-      grid = static_cast<int>(std::min<long long>(grid, fit));
+      if (fit < n_batches) grid = static_cast<int>(fit) * (cluster_mode ? cs : 1);
     }
   }
   o.grid = grid;
@@ -102,7 +125,8 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   o.layout = layout;
   DevBuf work, q, ex, st, ft, stt, jc, jt, jch, att, gp, gf, gb;
   const size_t nvals = static_cast<size_t>(std::max(1, P.n_e)) * P.n_t;
-  if ((ce = work.alloc(stride * (grid_mode ? 1 : grid) * sizeof(double2), s)) || (ce = q.alloc(8, s)) ||
+  if ((ce = work.alloc(stride * (grid_mode ? 1 : cluster_mode ? grid / cs : grid) * sizeof(double2), s)) ||
+      (ce = q.alloc(8, s)) ||
       (ce = ex.alloc(nvals * n_sys * sizeof(double2), s)) || (ce = st.alloc(sizeof(int) * n_sys, s)) ||
       (ce = ft.alloc(sizeof(double) * n_sys, s)) || (ce = stt.alloc(sizeof(long long) * 3 * n_sys, s)) ||
       (ce = jc.alloc(sizeof(int) * n_sys, s)) ||
@@ -131,7 +155,7 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   P.gfin = gf.as<double>();
   P.bar = gb.as<unsigned>();
   cudaEventRecord(ctx->ev[2], s);
-  if ((ce = launch_batch(P, layout, grid, s))) return cuda_fail(ce, "batch launch");
+  if ((ce = launch_batch(P, layout, grid, cs, s))) return cuda_fail(ce, "batch launch");
   cudaEventRecord(ctx->ev[3], s);
   o.expect.resize(nvals * n_sys);
   o.status.resize(n_sys);
@@ -169,7 +193,7 @@ qsg_status common_setup(qsg_ctx* ctx, const qsg_generator* G, long long n, const
     return QSG_UNSUPPORTED;
   }
   P.n = static_cast<int>(n);
-  P.gen = make_devgen(G, false);
+  P.gen = make_devgen(G, batch_codes());
   P.atol = opts ? opts->abstol : 1e-8;
   P.rtol = opts ? opts->reltol : 1e-6;
   if (!(P.atol > 0 && P.rtol > 0)) {

@@ -40,6 +40,42 @@ constexpr int NBUF = 12;
 enum Buf { Y = 0, YO, K1, K1O, K2, K3, K4, K5, K6, K7, SA, SB, Y1 = SA, SC = SB };
 enum Phase { FREE = 0, START, RUN, JUMP, OBS, FINISH, DONE };
 enum Src { SRC_DENSE = 0, SRC_Y = 1, SRC_SC = 2 };
+// Group modes: who shares one batch of slots.
+//   GM_CTA:     each CTA runs its own batch over all rows (block barriers only).
+//   GM_GRID:    one batch for the whole cooperative grid, rows partitioned over CTAs, passes
+//               separated by software grid barriers.
+//   GM_CLUSTER: one batch per thread-block cluster, rows partitioned over the cluster's CTAs,
+//               passes separated by hardware cluster barriers, slot reductions through DSMEM.
+enum GroupMode { GM_CTA = 0, GM_GRID = 1, GM_CLUSTER = 2 };
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+// loads from the shared memory of CTA `rank` of this cluster (DSMEM)
+__device__ __forceinline__ double dsmem_ld(const double* p, unsigned rank) {
+  unsigned la = static_cast<unsigned>(__cvta_generic_to_shared(p)), ra;
+  double v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rank));
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long dsmem_ld_u64(const unsigned long long* p, unsigned rank) {
+  unsigned la = static_cast<unsigned>(__cvta_generic_to_shared(p)), ra;
+  unsigned long long v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rank));
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ra) : "memory");
+  return v;
+}
 
 struct Slot {
   int phase, next_phase, after_obs;
@@ -200,8 +236,8 @@ __device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
 // GRID: the CTA totals go to gpart[value][rank]; the last CTA to arrive sums every value over the
 // CTAs in rank order (so the result does not depend on arrival order), publishes gfin and
 // releases the others. Every CTA then holds identical totals.
-template <int BS, bool GRID, int NA>
-__device__ void slot_reduce(const BatchProblem& P, double (&acc)[NA], double* sred, double* out) {
+template <int BS, int GM, int NA>
+__device__ void slot_reduce(const BatchProblem& P, double (&acc)[NA], double* sred, double* out, double* pub) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, s = lane % BS, rs = lane / BS;
 #pragma unroll
   for (int a = 0; a < NA; ++a)
@@ -218,7 +254,22 @@ __device__ void slot_reduce(const BatchProblem& P, double (&acc)[NA], double* sr
     out[ss * NA + a] = v;
   }
   __syncthreads();
-  if constexpr (GRID) {
+  if constexpr (GM == GM_CLUSTER) {
+    // every CTA publishes its totals in its own shared memory (double-buffered by the caller, so
+    // the next reduction cannot overwrite a buffer another CTA is still reading), then sums the
+    // cluster's totals in rank order: identical results in every CTA of the cluster.
+    const int cnt = BS * NA;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) pub[i] = out[i];
+    cluster_sync_all();
+    const unsigned cs = cluster_size();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      double v = 0.0;
+      for (unsigned r = 0; r < cs; ++r) v += dsmem_ld(pub + i, r);
+      out[i] = v;
+    }
+    __syncthreads();
+  }
+  if constexpr (GM == GM_GRID) {
     // two-phase distributed reduce: every CTA publishes its totals, then value i is summed over
     // the CTAs in rank order by one warp of CTA (i mod G); a second barrier publishes the result.
     const int G = gridDim.x, rank = blockIdx.x, cnt = BS * NA;
@@ -271,8 +322,11 @@ __device__ bool has_more(const Slot& s, const BatchProblem& P) {
 // BS slots per batch. !GRID: every CTA runs its own batch over all rows (block barriers only).
 // GRID: one batch for the whole cooperative grid, rows partitioned over CTAs, so the state of
 // the BS slots (NBUF x n x BS complex) stays L2-resident; passes are separated by grid barriers.
-template <int BS, bool GRID>
+template <int BS, int GM>
 __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const __grid_constant__ BatchProblem P) {
+  constexpr bool GRID = GM == GM_GRID;
+  constexpr bool CLU = GM == GM_CLUSTER;
+  constexpr bool PART = GM != GM_CTA;  // rows partitioned over the CTAs of a group
   constexpr int B = BS;
   constexpr int RPW = 32 / BS;
   __shared__ Slot S[BS];
@@ -281,24 +335,34 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
   __shared__ int s_alldone;
   __shared__ long long s_next;
   __shared__ unsigned char s_map[BS][NBUF];
+  __shared__ double s_pub[2][BS * 15];            // cluster mode: published CTA totals
+  __shared__ unsigned long long s_assign[BS];     // cluster mode: systems drawn by rank 0
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sl = lane % B, rs = lane / B;
   const int n = P.n;
-  const Ctx<BS> C{P, P.work + (GRID ? 0LL : static_cast<long long>(blockIdx.x) * P.work_stride), n, s_map};
+  const int g_rank = GRID ? static_cast<int>(blockIdx.x) : CLU ? static_cast<int>(cluster_rank()) : 0;
+  const int g_size = GRID ? static_cast<int>(gridDim.x) : CLU ? static_cast<int>(cluster_size()) : 1;
+  const long long batch_id = GRID ? 0LL : CLU ? static_cast<long long>(blockIdx.x) / g_size : blockIdx.x;
+  const Ctx<BS> C{P, P.work + batch_id * P.work_stride, n, s_map};
   const double atol = P.atol, rtol = P.rtol, eps_t = P.eps_t, tf = P.tf, t0 = P.t0;
-  const bool out_cta = !GRID || blockIdx.x == 0;  // the CTA that writes per-system outputs
-  const int rpc = GRID ? (n + gridDim.x - 1) / static_cast<int>(gridDim.x) : n;
-  const int r_lo = GRID ? min(n, static_cast<int>(blockIdx.x) * rpc) : 0;
-  const int r_hi = GRID ? min(n, r_lo + rpc) : n;
+  const bool out_cta = g_rank == 0;  // the CTA of a group that writes per-system outputs
+  const int rpc = PART ? (n + g_size - 1) / g_size : n;
+  const int r_lo = PART ? min(n, g_rank * rpc) : 0;
+  const int r_hi = PART ? min(n, r_lo + rpc) : n;
+  int pub_par = 0;
   auto rows = [&](auto&& f) {
     for (int r = r_lo + warp * RPW + rs; r < r_hi; r += W * RPW) f(r);
   };
   auto pass_sync = [&]() {
     if constexpr (GRID) grid_barrier(P.bar, gridDim.x);
+    else if constexpr (CLU) cluster_sync_all();
     else __syncthreads();
   };
-  auto reduce = [&](auto& acc) { slot_reduce<BS, GRID>(P, acc, sred, sout); };
+  auto reduce = [&](auto& acc) {
+    slot_reduce<BS, GM>(P, acc, sred, sout, s_pub[pub_par]);
+    pub_par ^= 1;
+  };
 
   if (threadIdx.x < B) {
     S[threadIdx.x].phase = FREE;
@@ -314,12 +378,22 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         if (S[b].phase == FREE) S[b].sys = s_next < P.n_systems ? s_next++ : -1;
     }
     if (GRID) __syncthreads();
+    if constexpr (CLU) {  // rank 0 draws the next systems from the queue, the cluster reads them
+      bool anyfree = false;
+      for (int b = 0; b < B; ++b) anyfree |= S[b].phase == FREE;
+      if (anyfree) {
+        if (g_rank == 0 && threadIdx.x < B && S[threadIdx.x].phase == FREE)
+          s_assign[threadIdx.x] = atomicAdd(P.queue, 1ull);
+        cluster_sync_all();
+      }
+    }
     if (threadIdx.x < B) {
       Slot& s = S[threadIdx.x];
       s.fresh = 0;
       if (s.phase == FREE) {
         unsigned long long idx;
         if (GRID) idx = s.sys < 0 ? ~0ull : static_cast<unsigned long long>(s.sys);
+        else if (CLU) idx = dsmem_ld_u64(&s_assign[threadIdx.x], 0);
         else idx = atomicAdd(P.queue, 1ull);
         if (idx < static_cast<unsigned long long>(P.n_systems)) {
           s.sys = static_cast<long long>(idx);
@@ -459,8 +533,8 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
             });
           } else {  // sum A(i,j) rho_h(j,i) (evolve.cpp:286-295)
             const int beg = P.eo_off[e], end = P.eo_off[e + 1];
-            const int r0 = GRID ? beg + (end - beg) * static_cast<long long>(blockIdx.x) / gridDim.x : beg;
-            const int r1 = GRID ? beg + (end - beg) * static_cast<long long>(blockIdx.x + 1) / gridDim.x : end;
+            const int r0 = PART ? beg + (end - beg) * static_cast<long long>(g_rank) / g_size : beg;
+            const int r1 = PART ? beg + (end - beg) * static_cast<long long>(g_rank + 1) / g_size : end;
             for (int k = r0 + warp * RPW + rs; k < r1; k += W * RPW) {
               const int i = P.eo_i[k], j = P.eo_j[k];
               const double2 rji = dense_at(C, i * P.d + j, sl, th, hl, src);
@@ -836,66 +910,135 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
     }
     __syncthreads();
   }
+  // no CTA may leave while another still reads its shared memory (reductions, rank 0's draws)
+  if constexpr (CLU) cluster_sync_all();
 }
 
-template <int BS, bool GRID>
+template <int BS, int GM>
 size_t dyn_smem() {
   return static_cast<size_t>(W) * BS * 15 * sizeof(double);
 }
 
-template <int BS, bool GRID>
+template <int BS, int GM>
 void set_attrs() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(batch_kernel<BS, GRID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(dyn_smem<BS, GRID>()));
+    cudaFuncSetAttribute(batch_kernel<BS, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(dyn_smem<BS, GM>()));
+    if (GM == GM_CLUSTER) cudaFuncSetAttribute(batch_kernel<BS, GM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     done = true;
   }
 }
 
-template <int BS, bool GRID>
+template <int BS, int GM>
 int occupancy_of() {
-  set_attrs<BS, GRID>();
+  set_attrs<BS, GM>();
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, batch_kernel<BS, GRID>, kThreads, dyn_smem<BS, GRID>());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, batch_kernel<BS, GM>, kThreads, dyn_smem<BS, GM>());
   return nb;
+}
+
+template <int BS>
+cudaError_t launch_cluster(const BatchProblem& P, int grid, int cs, cudaStream_t s) {
+  set_attrs<BS, GM_CLUSTER>();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = dyn_smem<BS, GM_CLUSTER>();
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, batch_kernel<BS, GM_CLUSTER>, P);
+}
+
+template <int BS>
+int cluster_capacity(int cs) {
+  set_attrs<BS, GM_CLUSTER>();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs * 64);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = dyn_smem<BS, GM_CLUSTER>();
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, batch_kernel<BS, GM_CLUSTER>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return nc;
 }
 
 }  // namespace
 
-// layouts: 0 = per-CTA batches of 8 slots, 1 = grid-wide batch of 32 slots, 2 = per-CTA batches of
-// 4 slots (fills the GPU with half as many trajectories as layout 0)
-int batch_slots(int layout) { return layout == 1 ? kMaxB : layout == 2 ? 4 : layout == 3 ? 2 : layout == 4 ? 1 : 8; }
+// layouts: 0/2/3/4 = per-CTA batches of 8/4/2/1 slots, 1 = grid-wide batch of 32 slots,
+// 5/6 = per-cluster batches of 1/2 slots
+int batch_slots(int layout) {
+  switch (layout) {
+    case 1: return kMaxB;
+    case 2: return 4;
+    case 3: return 2;
+    case 4: return 1;
+    case 5: return 1;
+    case 6: return 2;
+    default: return 8;
+  }
+}
 
 size_t batch_work_stride(int n, int layout) {
   return static_cast<size_t>(NBUF) * static_cast<size_t>(n) * batch_slots(layout);
 }
 
 int batch_max_blocks_per_sm(int layout) {
-  return layout == 1 ? occupancy_of<kMaxB, true>() : layout == 2 ? occupancy_of<4, false>()
-         : layout == 3 ? occupancy_of<2, false>() : layout == 4 ? occupancy_of<1, false>()
-         : occupancy_of<8, false>();
+  switch (layout) {
+    case 1: return occupancy_of<kMaxB, GM_GRID>();
+    case 2: return occupancy_of<4, GM_CTA>();
+    case 3: return occupancy_of<2, GM_CTA>();
+    case 4: return occupancy_of<1, GM_CTA>();
+    case 5: return occupancy_of<1, GM_CLUSTER>();
+    case 6: return occupancy_of<2, GM_CLUSTER>();
+    default: return occupancy_of<8, GM_CTA>();
+  }
 }
 
-cudaError_t launch_batch(const BatchProblem& P, int layout, int grid, cudaStream_t s) {
-  if (layout == 1) {
-    void* args[] = {const_cast<BatchProblem*>(&P)};
-    set_attrs<kMaxB, true>();
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(batch_kernel<kMaxB, true>), dim3(grid),
-                                       dim3(kThreads), args, dyn_smem<kMaxB, true>(), s);
-  }
-  if (layout == 2) {
-    set_attrs<4, false>();
-    batch_kernel<4, false><<<grid, kThreads, dyn_smem<4, false>(), s>>>(P);
-  } else if (layout == 4) {
-    set_attrs<1, false>();
-    batch_kernel<1, false><<<grid, kThreads, dyn_smem<1, false>(), s>>>(P);
-  } else if (layout == 3) {
-    set_attrs<2, false>();
-    batch_kernel<2, false><<<grid, kThreads, dyn_smem<2, false>(), s>>>(P);
-  } else {
-    set_attrs<8, false>();
-    batch_kernel<8, false><<<grid, kThreads, dyn_smem<8, false>(), s>>>(P);
+int batch_max_clusters(int layout, int cs) {
+  return layout == 5 ? cluster_capacity<1>(cs) : layout == 6 ? cluster_capacity<2>(cs) : 0;
+}
+
+cudaError_t launch_batch(const BatchProblem& P, int layout, int grid, int cs, cudaStream_t s) {
+  switch (layout) {
+    case 1: {
+      void* args[] = {const_cast<BatchProblem*>(&P)};
+      set_attrs<kMaxB, GM_GRID>();
+      return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(batch_kernel<kMaxB, GM_GRID>), dim3(grid),
+                                         dim3(kThreads), args, dyn_smem<kMaxB, GM_GRID>(), s);
+    }
+    case 5: return launch_cluster<1>(P, grid, cs, s);
+    case 6: return launch_cluster<2>(P, grid, cs, s);
+    case 2:
+      set_attrs<4, GM_CTA>();
+      batch_kernel<4, GM_CTA><<<grid, kThreads, dyn_smem<4, GM_CTA>(), s>>>(P);
+      break;
+    case 3:
+      set_attrs<2, GM_CTA>();
+      batch_kernel<2, GM_CTA><<<grid, kThreads, dyn_smem<2, GM_CTA>(), s>>>(P);
+      break;
+    case 4:
+      set_attrs<1, GM_CTA>();
+      batch_kernel<1, GM_CTA><<<grid, kThreads, dyn_smem<1, GM_CTA>(), s>>>(P);
+      break;
+    default:
+      set_attrs<8, GM_CTA>();
+      batch_kernel<8, GM_CTA><<<grid, kThreads, dyn_smem<8, GM_CTA>(), s>>>(P);
   }
   return cudaGetLastError();
 }

@@ -58,7 +58,9 @@ struct BatchProblem {
 };
 
 int batch_slots(int layout);
-cudaError_t launch_batch(const BatchProblem& P, int layout, int grid, cudaStream_t s);
+// cs: CTAs per cluster (cluster layouts 5/6 only); grid must then be a multiple of cs
+cudaError_t launch_batch(const BatchProblem& P, int layout, int grid, int cs, cudaStream_t s);
+int batch_max_clusters(int layout, int cs);  // co-resident clusters of cs CTAs
 int batch_max_blocks_per_sm(int layout);
 size_t batch_work_stride(int n, int layout);  // double2 elements per batch
 

@@ -127,12 +127,13 @@ def test_mesolve_batch_sweep_parity(ctx):
         assert_stats_close(res["stats"][p], st)
 
 
-MODES = ["local1", "local2", "local4", "local", "grid"]
+MODES = ["local1", "local2", "local4", "local", "grid", "cluster1", "cluster2"]
 
 
 @pytest.fixture(params=MODES)
 def batch_mode(request, monkeypatch):
-    """Every batch-engine layout: 1/2/4/8 slots per CTA and the grid-wide 32-slot batch."""
+    """Every batch-engine layout: 1/2/4/8 slots per CTA, the grid-wide 32-slot batch and 1/2 slots
+    per 16-CTA cluster."""
     monkeypatch.setenv("QSG_BATCH_MODE", request.param)
     return request.param
 
