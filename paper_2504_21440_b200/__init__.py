@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libqsim_b200.so")
+LIB_PATH = os.environ.get("QSG_LIB_PATH") or os.path.join(_PKG, "lib", "libqsim_b200.so")
 _lib = None
 
 P = C.c_void_p

@@ -145,6 +145,96 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
 
 // One row of a SELL-32 operator times a gathered vector (lane-per-row). XF maps col -> x[col].
 // Entries are consumed in ascending column order, as Eigen's CSC product accumulates a row.
+// Register-resident view of a coded store's streams (kernel-parameter fields would otherwise be
+// re-read from the constant bank at every entry).
+struct CodedView {
+  const unsigned char* __restrict__ code8;
+  const unsigned short* __restrict__ code16;
+  const double2* __restrict__ dval;
+  const int* __restrict__ doff;
+  int cbytes;
+};
+__device__ __forceinline__ CodedView coded_view(const DevSell& A) {
+  CodedView v{A.code8, A.code16, A.dict_val, A.dict_off, A.code_bytes};
+  __builtin_assume(__isGlobal(v.dval));
+  __builtin_assume(__isGlobal(v.doff));
+  return v;
+}
+
+// Coded row through a CodedView: `len` entries whose codes start at offset `base`.
+template <class XF>
+__device__ __forceinline__ double2 sell_row_coded_v(const CodedView& A, int row, int len, long long base, XF&& xf) {
+  double2 acc = make_double2(0.0, 0.0);
+  for (int j0 = 0; j0 < len; j0 += 32) {
+    uint4 w[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + 8 * c;
+      if (j < len) {
+        if (A.cbytes == 1) {
+          const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + j));
+          w[c] = make_uint4(v.x, v.y, 0u, 0u);
+        } else {
+          w[c] = ld_stream_u4(reinterpret_cast<const uint4*>(A.code16 + base + j));
+        }
+      } else {
+        w[c] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + 8 * c + u;
+        if (j < len) {
+          unsigned k;
+          if (A.cbytes == 1) k = ((u < 4 ? w[c].x : w[c].y) >> (8 * (u & 3))) & 0xffu;
+          else k = ((u < 2 ? w[c].x : u < 4 ? w[c].y : u < 6 ? w[c].z : w[c].w) >> (16 * (u & 1))) & 0xffffu;
+          cfma(__ldg(A.dval + k), xf(row + __ldg(A.doff + k)), acc);
+        }
+      }
+  }
+  return acc;
+}
+
+// Coded-store row with its metadata already loaded: `len` entries whose codes start at byte (or
+// uint16) offset `base`. The row's codes are contiguous (a multiple of 8 per row), so 8 codes come
+// in one 8 B (uint8) or 16 B (uint16) load and a 32-entry row is in flight after 4 loads.
+template <class XF>
+__device__ __forceinline__ double2 sell_row_coded(const DevSell& A, int row, int len, long long base, XF&& xf) {
+  double2 acc = make_double2(0.0, 0.0);
+  for (int j0 = 0; j0 < len; j0 += 32) {
+    uint4 w[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + 8 * c;
+      if (j < len) {
+        if (A.code_bytes == 1) {
+          const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + j));
+          w[c] = make_uint4(v.x, v.y, 0u, 0u);
+        } else {
+          w[c] = ld_stream_u4(reinterpret_cast<const uint4*>(A.code16 + base + j));
+        }
+      } else {
+        w[c] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + 8 * c + u;
+        if (j < len) {
+          unsigned k;
+          if (A.code_bytes == 1) k = ((u < 4 ? w[c].x : w[c].y) >> (8 * (u & 3))) & 0xffu;
+          else k = ((u < 2 ? w[c].x : u < 4 ? w[c].y : u < 6 ? w[c].z : w[c].w) >> (16 * (u & 1))) & 0xffffu;
+          cfma(__ldg(A.dict_val + k), xf(row + __ldg(A.dict_off + k)), acc);
+        }
+      }
+  }
+  return acc;
+}
+
 template <class XF>
 __device__ __forceinline__ double2 sell_row(const DevSell& A, int slice, int lane, XF&& xf) {
   const int len = __ldg(A.rowlen + slice * 32 + lane);
@@ -170,40 +260,9 @@ __device__ __forceinline__ double2 sell_row(const DevSell& A, int slice, int lan
         if (j + u < len) cfma(v[u], xf(c[u]), acc);
     }
   } else {
-    // coded store: the row's codes are contiguous (Wp per row, a multiple of 8), so 8 codes come
-    // in one 8 B (uint8) or 16 B (uint16) load and a 32-entry row is in flight after 4 loads
     const long long cb = __ldg(A.code_off + slice);
     const int wp = static_cast<int>((__ldg(A.code_off + slice + 1) - cb) >> 5);
-    const long long base = cb + static_cast<long long>(lane) * wp;
-    for (int j0 = 0; j0 < len; j0 += 32) {
-      uint4 w[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int j = j0 + 8 * c;
-        if (j < len) {
-          if (A.code_bytes == 1) {
-            const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + j));
-            w[c] = make_uint4(v.x, v.y, 0u, 0u);
-          } else {
-            w[c] = ld_stream_u4(reinterpret_cast<const uint4*>(A.code16 + base + j));
-          }
-        } else {
-          w[c] = make_uint4(0u, 0u, 0u, 0u);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int j = j0 + 8 * c + u;
-          if (j < len) {
-            unsigned k;
-            if (A.code_bytes == 1) k = ((u < 4 ? w[c].x : w[c].y) >> (8 * (u & 3))) & 0xffu;
-            else k = ((u < 2 ? w[c].x : u < 4 ? w[c].y : u < 6 ? w[c].z : w[c].w) >> (16 * (u & 1))) & 0xffffu;
-            cfma(__ldg(A.dict_val + k), xf(row + __ldg(A.dict_off + k)), acc);
-          }
-        }
-    }
+    acc = sell_row_coded(A, row, len, cb + static_cast<long long>(lane) * wp, xf);
   }
   return acc;
 }

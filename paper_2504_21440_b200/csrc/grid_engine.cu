@@ -23,7 +23,10 @@ namespace qsg {
 
 namespace {
 
-constexpr int kThreads = 512;
+#ifndef QSG_GRID_THREADS
+#define QSG_GRID_THREADS 512
+#endif
+constexpr int kThreads = QSG_GRID_THREADS;
 #ifndef QSG_GRID_MINB
 #define QSG_GRID_MINB 2
 #endif
@@ -173,6 +176,10 @@ __device__ __forceinline__ void push_pending(const GridProblem& P, Ctl& c, doubl
 // PF: load the epilogue operands before the SpMV (their HBM latency then overlaps the gathers).
 // Used with the dictionary-coded store, whose SpMV needs few registers; with the plain store the
 // extra live registers spill, so the operands are loaded after the SpMV instead.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <int S, bool PF>
 __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c, int s0, int s1) {
   using namespace dp;
@@ -181,57 +188,69 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
   const double hh = c.hh;
   const double ts = S == 2 ? c.t + c2 * hh : S == 3 ? c.t + c3 * hh : S == 4 ? c.t + c4 * hh
                   : S == 5 ? c.t + c5 * hh : c.t + hh;
-  const double2* __restrict__ y = c.p[Y];
-  const double2* __restrict__ k1 = c.p[K1];
-  const double2* __restrict__ x = S == 2 ? nullptr : (S == 3 || S == 5 || S == 7) ? c.p[SA] : c.p[SB];
+  // every buffer pointer is read from the shared control block once per pass and kept in a
+  // restrict-qualified global pointer: stores through them cannot alias the control block, so the
+  // loop neither re-reads it nor issues generic loads
+  auto gptr = [](double2* p) {
+    __builtin_assume(__isGlobal(p));
+    return p;
+  };
+  const double2* __restrict__ y = gptr(c.p[Y]);
+  const double2* __restrict__ k1 = gptr(c.p[K1]);
+  const double2* __restrict__ x = S == 2 ? nullptr : gptr((S == 3 || S == 5 || S == 7) ? c.p[SA] : c.p[SB]);
+  const double2* __restrict__ pk2 = gptr(c.p[K2]);
+  const double2* __restrict__ pk3 = gptr(c.p[K3]);
+  const double2* __restrict__ pk4 = gptr(c.p[K4]);
+  const double2* __restrict__ pk5 = gptr(c.p[K5]);
+  const double2* __restrict__ pk6 = gptr(c.p[K6]);
+  double2* __restrict__ kout = gptr(c.p[S == 2 ? K2 : S == 3 ? K3 : S == 4 ? K4 : S == 5 ? K5 : S == 6 ? K6 : K7]);
+  double2* __restrict__ xout = gptr(c.p[(S == 3 || S == 5) ? SB : SA]);
   double esq = 0.0;
   const double2 z = make_double2(0.0, 0.0);
-  for (int b = s0 + warp; b < s1; b += W) {
-    const int row = (b << 5) + lane;
-    const bool ok = row < n;
+  struct Ops {
     double2 yy, q1, q2, q3, q4, q5, q6, y1;
-    auto load_operands = [&]() {
-      yy = ok ? y[row] : z;
-      q1 = ok ? k1[row] : z;
-      q2 = (S >= 3 && S <= 5 && ok) ? c.p[K2][row] : z;
-      q3 = (S >= 4 && ok) ? c.p[K3][row] : z;
-      q4 = (S >= 5 && ok) ? c.p[K4][row] : z;
-      q5 = (S >= 6 && ok) ? c.p[K5][row] : z;
-      q6 = (S == 7 && ok) ? c.p[K6][row] : z;
-      y1 = (S == 7 && ok) ? x[row] : z;
-    };
-    if (PF) load_operands();
-    double2 k;
-    if (S == 2)
-      k = gen_row(P.gen, P.params, b, ts, [&](int col) {
-        const double2 a = y[col], q = k1[col];
-        return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
-      });
-    else
-      k = gen_row(P.gen, P.params, b, ts, [&](int col) { return x[col]; });
-    if (!ok) continue;
-    if (!PF) load_operands();
+  };
+  auto load_operands = [&](int row, bool ok, Ops& o) {
+    o.yy = ok ? y[row] : z;
+    o.q1 = ok ? k1[row] : z;
+    o.q2 = (S >= 3 && S <= 5 && ok) ? pk2[row] : z;
+    o.q3 = (S >= 4 && ok) ? pk3[row] : z;
+    o.q4 = (S >= 5 && ok) ? pk4[row] : z;
+    o.q5 = (S >= 6 && ok) ? pk5[row] : z;
+    o.q6 = (S == 7 && ok) ? pk6[row] : z;
+    o.y1 = (S == 7 && ok) ? x[row] : z;
+  };
+  auto xin = [&](int col) {
+    if constexpr (S == 2) {
+      const double2 a = y[col], q = k1[col];
+      return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
+    } else {
+      return x[col];
+    }
+  };
+  auto epilogue = [&](int row, double2 k, const Ops& o) {
+    const double2 yy = o.yy, q1 = o.q1, q2 = o.q2, q3 = o.q3, q4 = o.q4, q5 = o.q5, q6 = o.q6, y1 = o.y1;
     if (S == 2) {
-      c.p[K2][row] = k;
-      c.p[SA][row] = make_double2(yy.x + hh * (a31 * q1.x + a32 * k.x), yy.y + hh * (a31 * q1.y + a32 * k.y));
+      kout[row] = k;
+      xout[row] = make_double2(yy.x + hh * (a31 * q1.x + a32 * k.x), yy.y + hh * (a31 * q1.y + a32 * k.y));
     } else if (S == 3) {
-      c.p[K3][row] = k;
-      c.p[SB][row] = make_double2(yy.x + hh * (a41 * q1.x + a42 * q2.x + a43 * k.x),
+      kout[row] = k;
+      xout[row] = make_double2(yy.x + hh * (a41 * q1.x + a42 * q2.x + a43 * k.x),
                                   yy.y + hh * (a41 * q1.y + a42 * q2.y + a43 * k.y));
     } else if (S == 4) {
-      c.p[K4][row] = k;
-      c.p[SA][row] = make_double2(yy.x + hh * (a51 * q1.x + a52 * q2.x + a53 * q3.x + a54 * k.x),
+      kout[row] = k;
+      xout[row] = make_double2(yy.x + hh * (a51 * q1.x + a52 * q2.x + a53 * q3.x + a54 * k.x),
                                   yy.y + hh * (a51 * q1.y + a52 * q2.y + a53 * q3.y + a54 * k.y));
     } else if (S == 5) {
-      c.p[K5][row] = k;
-      c.p[SB][row] = make_double2(yy.x + hh * (a61 * q1.x + a62 * q2.x + a63 * q3.x + a64 * q4.x + a65 * k.x),
+      kout[row] = k;
+      xout[row] = make_double2(yy.x + hh * (a61 * q1.x + a62 * q2.x + a63 * q3.x + a64 * q4.x + a65 * k.x),
                                   yy.y + hh * (a61 * q1.y + a62 * q2.y + a63 * q3.y + a64 * q4.y + a65 * k.y));
     } else if (S == 6) {
-      c.p[K6][row] = k;
-      c.p[SA][row] = make_double2(yy.x + hh * (a71 * q1.x + a73 * q3.x + a74 * q4.x + a75 * q5.x + a76 * k.x),
+      kout[row] = k;
+      xout[row] = make_double2(yy.x + hh * (a71 * q1.x + a73 * q3.x + a74 * q4.x + a75 * q5.x + a76 * k.x),
                                   yy.y + hh * (a71 * q1.y + a73 * q3.y + a74 * q4.y + a75 * q5.y + a76 * k.y));
     } else {
-      c.p[K7][row] = k;
+      kout[row] = k;
       double2 e;
       e.x = hh * (e1 * q1.x + e3 * q3.x + e4 * q4.x + e5 * q5.x + e6 * q6.x + e7 * k.x);
       e.y = hh * (e1 * q1.y + e3 * q3.y + e4 * q4.y + e5 * q5.y + e6 * q6.y + e7 * k.y);
@@ -239,6 +258,71 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
       const double qq = cabs_(e) / sc;
       esq += qq * qq;
     }
+  };
+  if constexpr (PF) {
+    if (P.gen.n_terms == 1) {
+      // Software-pipelined coded SpMV: the next slice's row metadata is loaded at the top of the
+      // iteration, and its codes and epilogue operands are prefetched into L2 once that metadata
+      // is in, so each slice waits on one L2 round trip (the x gathers) instead of three
+      // (metadata, HBM codes, gathers).
+      const DevSell& A = P.gen.A[0];
+      const CodedView cv = coded_view(A);
+      const int* __restrict__ rowlen = A.rowlen;
+      const long long* __restrict__ code_off = A.code_off;
+      auto meta = [&](int b, int& len, long long& base) {
+        len = __ldg(rowlen + b * 32 + lane);
+        const long long cb = __ldg(code_off + b);
+        const int wp = static_cast<int>((__ldg(code_off + b + 1) - cb) >> 5);
+        base = cb + static_cast<long long>(lane) * wp;
+      };
+      int b = s0 + warp, len = 0;
+      long long base = 0;
+      if (b < s1) meta(b, len, base);
+      for (; b < s1; b += W) {
+        const int bn = b + W;
+        int len_n = 0;
+        long long base_n = 0;
+        if (bn < s1) meta(bn, len_n, base_n);
+        const int row = (b << 5) + lane;
+        const bool ok = row < n;
+        Ops o;
+        load_operands(row, ok, o);
+        const double2 k = sell_row_coded_v(cv, row, len, base, xin);
+        if (bn < s1) {
+          const char* cp = cv.cbytes == 1 ? reinterpret_cast<const char*>(cv.code8 + base_n)
+                                          : reinterpret_cast<const char*>(cv.code16 + base_n);
+          prefetch_l2(cp);
+          if (len_n * cv.cbytes > 32) prefetch_l2(cp + len_n * cv.cbytes - 1);
+          const int rn = (bn << 5) + lane;
+          if (rn < n) {
+            prefetch_l2(y + rn);
+            prefetch_l2(k1 + rn);
+            if (S >= 3 && S <= 5) prefetch_l2(pk2 + rn);
+            if (S >= 4) prefetch_l2(pk3 + rn);
+            if (S >= 5) prefetch_l2(pk4 + rn);
+            if (S >= 6) prefetch_l2(pk5 + rn);
+            if (S == 7) {
+              prefetch_l2(pk6 + rn);
+              prefetch_l2(x + rn);
+            }
+          }
+        }
+        if (ok) epilogue(row, k, o);
+        len = len_n;
+        base = base_n;
+      }
+      return esq;
+    }
+  }
+  for (int b = s0 + warp; b < s1; b += W) {
+    const int row = (b << 5) + lane;
+    const bool ok = row < n;
+    Ops o;
+    if (PF) load_operands(row, ok, o);
+    const double2 k = gen_row(P.gen, P.params, b, ts, xin);
+    if (!ok) continue;
+    if (!PF) load_operands(row, ok, o);
+    epilogue(row, k, o);
   }
   return esq;
 }
