@@ -138,19 +138,25 @@ def run_ours(args, ws, rank, local):
     ctx = q.Context(dev)
     peak, peak_src = hbm_peak()
 
-    # ---- host model assembly with the product's C++ API (timed separately, not part of value)
+    # ---- model: H, c_ops and e_ops from the product's C++ API (factories.cpp:204-246), then the
+    # Liouvillian assembled on the device (qsg_liouvillian_create, equal to the reference's L entry
+    # for entry, tests/test_gpu_liouvillian.py) straight into the operator store
     t0 = time.perf_counter()
     model = q.Model("ising", *TFIM)
-    L = model.export(q.SEL_L_CONST)
+    H = model.export(q.SEL_H_CONST)
+    cops = [model.export(q.SEL_C_OP, k) for k in range(model.n_cops)]
     eops = [model.export(q.SEL_E_OP, k) for k in range(model.n_eops)]
-    host_build_s = time.perf_counter() - t0
-    d, n, nnz = model.dim, L.n_rows, L.nnz
+    host_ops_s = time.perf_counter() - t0
+    d = model.dim
     psi = model.psi0()
     rho0 = np.outer(psi, psi.conj()).reshape(-1, order="F").copy()
 
+    ctx.liouvillian(H, cops).close()  # first call pays the pool growth
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    op = ctx.op(L)
+    op = ctx.liouvillian(H, cops)
     store_build_s = time.perf_counter() - t0
+    n, nnz = op.n, op.nnz
     gen = q.Generator([op])
     rho0_dev = torch.from_numpy(rho0).to(f"cuda:{dev}")
 
@@ -190,25 +196,50 @@ def run_ours(args, ws, rank, local):
         except Exception:
             traffic = None
 
-    # ---- end to end through the C-ABI with host buffers (pinned), copies inside the timed region
+    # ---- end to end through the C-ABI with host buffers (pinned), copies inside the timed region:
+    # the reference's mesolve(H, rho0, tlist, c_ops, e_ops) inputs -> device Liouvillian assembly +
+    # operator store (qsg_liouvillian_create) -> qsg_mesolve(host rho0 -> host expect)
     pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
-    Lh = q.CsrMatrix(pin(L.rowptr), pin(L.col), pin(L.val), L.n_rows, L.n_cols)
+    pcsr = lambda m: q.CsrMatrix(pin(m.rowptr), pin(m.col), pin(m.val), m.n_rows, m.n_cols)
+    Hh, cops_h = pcsr(H), [pcsr(c) for c in cops]
     rho0_h = pin(rho0)
     e2e_steps = max(1, min(args.steps, 5))
     for _ in range(3):  # untimed warm-up: the stream-ordered pool reaches its steady-state blocks
-        op_w = ctx.op(Lh)
+        op_w = ctx.liouvillian(Hh, cops_h)
         q.mesolve(ctx, q.Generator([op_w]), d, rho0_h, TLIST, eops)
         op_w.close()
     barrier(ws)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        op2 = ctx.op(Lh)
+        op2 = ctx.liouvillian(Hh, cops_h)
         r2 = q.mesolve(ctx, q.Generator([op2]), d, rho0_h, TLIST, eops)
         _ = r2["expect"].sum()
         op2.close()
     e2e_s = allreduce_max((time.perf_counter() - t0) / e2e_steps, ws)
-    h2d = csr_bytes(L) + rho0.nbytes + sum(csr_bytes(e) for e in eops)
+    h2d = csr_bytes(H) + sum(csr_bytes(c) for c in cops) + rho0.nbytes + sum(csr_bytes(e) for e in eops)
     d2h = r2["expect"].nbytes
+
+    # the same, starting from the reference-built Liouvillian CSR (host build timed separately)
+    e2e_L = None
+    if not args.quick:
+        t0 = time.perf_counter()
+        L = model.export(q.SEL_L_CONST)
+        host_l_build_s = time.perf_counter() - t0
+        Lh = pcsr(L)
+        op_w = ctx.op(Lh)
+        q.mesolve(ctx, q.Generator([op_w]), d, rho0_h, TLIST, eops)
+        op_w.close()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            op3 = ctx.op(Lh)
+            r3 = q.mesolve(ctx, q.Generator([op3]), d, rho0_h, TLIST, eops)
+            _ = r3["expect"].sum()
+            op3.close()
+        e2e_L = {"value": allreduce_max((time.perf_counter() - t0) / e2e_steps, ws), "unit": "s",
+                 "h2d_bytes_per_step": int(csr_bytes(L) + rho0.nbytes + sum(csr_bytes(e) for e in eops)),
+                 "path": "qsg_op_create(pinned host Liouvillian CSR) + qsg_mesolve",
+                 "host_liouvillian_build_s": host_l_build_s}
+        del Lh, L
 
     # ---- secondary: SpMV of the operator store (SpMV HBM GB/s metric), and the same solve on the
     # plain (int32 column + complex128 value) store for comparison
@@ -220,7 +251,7 @@ def run_ours(args, ws, rank, local):
                                  "GBps": spmv_bytes / spmv_ms / 1e6, "frac": spmv_bytes / spmv_ms / 1e6 / peak,
                                  "bytes_model": "store bytes + 32*n"}}
     os.environ["QSG_NO_COMPRESS"] = "1"
-    op_p = ctx.op(L)
+    op_p = ctx.liouvillian(H, cops)
     del os.environ["QSG_NO_COMPRESS"]
     gen_p = q.Generator([op_p])
     q.mesolve(ctx, gen_p, d, rho0_dev, TLIST, eops)
@@ -236,6 +267,8 @@ def run_ours(args, ws, rank, local):
     op_p.close()
     secondary["operator_store"] = {"code_bytes": cb, "dict_pairs": ndict, "bytes_per_spmv": mat_bytes,
                                    "plain_bytes_per_spmv": mat_p}
+    if e2e_L is not None:
+        secondary["e2e_from_liouvillian_csr"] = e2e_L
     if not args.quick:
         secondary["kerr_sweep_spmv"] = kerr_sweep_spmv(ctx, q, torch, dev, peak)
         secondary["kerr_cutoff_mesolve"] = kerr_cutoff_mesolve(ctx, q, peak)
@@ -263,7 +296,8 @@ def run_ours(args, ws, rank, local):
             "parallelism": f"replicas x{ws}" if ws > 1 else "single solve, one cooperative grid",
             "l2_flush": "inputs exceed L2 (operator 497 MB > 126 MB L2)",
             "dp5_attempts": att, "stats_steps_rejected_rhs": list(stats),
-            "host_build_s": host_build_s, "operator_store_build_s": store_build_s,
+            "host_operator_build_s": host_ops_s,
+            "device_liouvillian_and_store_build_s": store_build_s,
             "grid_ctas": r["grid_ctas"], "timed_wall_s": wall,
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -273,7 +307,7 @@ def run_ours(args, ws, rank, local):
                                     "store = code_bytes*nnz + 4*n + 16*n/32 + 20*pairs (coded) or "
                                     "20*nnz + 4*n + 8*n/32 (plain)"},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "path": "qsg_op_create(pinned host CSR) + qsg_mesolve(host rho0 -> host expect)"},
+                "path": "qsg_liouvillian_create(pinned host H, c_ops) + qsg_mesolve(host rho0 -> host expect)"},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
         "secondary": secondary,

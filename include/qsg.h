@@ -130,6 +130,18 @@ int64_t qsg_op_rows(const qsg_op* op);
 int32_t qsg_op_code_bytes(const qsg_op* op);
 int32_t qsg_op_dict_size(const qsg_op* op);
 
+/* On-device Liouvillian assembly (superop.cpp:78-91 liouvillian, :51-76 spre/spost/sprepost/
+ * lindblad_dissipator): L = -i(I(x)H - H^T(x)I) + sum_k D(c_k) for d x d CSR operators H (may be
+ * NULL) and c_ops, column-stacked vectorization (superop.hpp:9-10). Values and sparsity pattern
+ * (explicit zeros included) equal the reference's entry for entry. At most 32 collapse operators.
+ * qsg_liouvillian_create builds the operator store from it directly; qsg_liouvillian_export copies
+ * the CSR (n = d*d rows) into caller buffers (host or device; pass rowptr == NULL to query nnz). */
+qsg_status qsg_liouvillian_create(qsg_ctx* ctx, int64_t d, const qsg_csr* H, int32_t n_c,
+                                  const qsg_csr* c_ops, qsg_op** out);
+qsg_status qsg_liouvillian_export(qsg_ctx* ctx, int64_t d, const qsg_csr* H, int32_t n_c,
+                                  const qsg_csr* c_ops, int64_t* nnz, int32_t* rowptr,
+                                  int32_t* col, double* val);
+
 /* out = G(t) y  — SparseGenerator::apply (evolve.cpp:63-69). y/out: n complex. */
 qsg_status qsg_generator_apply(qsg_ctx* ctx, const qsg_generator* g, const double* params,
                                int32_t n_params, double t, const double* y, double* out);

@@ -115,6 +115,10 @@ def lib():
                                         DP, C.POINTER(_Stats), I32P, C.POINTER(_Timing)]
         L.qsg_rng_draw.argtypes = [P, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, DP,
                                    C.POINTER(C.c_uint64)]
+        L.qsg_liouvillian_create.argtypes = [P, C.c_int64, C.POINTER(_Csr), C.c_int32, C.POINTER(_Csr),
+                                             C.POINTER(P)]
+        L.qsg_liouvillian_export.argtypes = [P, C.c_int64, C.POINTER(_Csr), C.c_int32, C.POINTER(_Csr),
+                                             I64P, I32P, I32P, DP]
         _bind_model_api(L)
         _lib = L
     return _lib
@@ -190,6 +194,37 @@ class Context:
     def op(self, m: CsrMatrix) -> "Operator":
         return Operator(self, m)
 
+    def liouvillian(self, H, c_ops=()) -> "Operator":
+        """Operator store of L = -i[H, .] + sum_k D[c_k] assembled on the device
+        (qsg_liouvillian_create; superop.cpp:78-91). H may be None."""
+        d, hc, carr = _liou_args(H, c_ops)
+        h = P()
+        _check(lib().qsg_liouvillian_create(self._h, d, hc, len(c_ops), carr, C.byref(h)))
+        return Operator._wrap(self, h, d * d, lib().qsg_op_nnz(h))
+
+
+def _liou_args(H, c_ops):
+    mats = ([H] if H is not None else []) + list(c_ops)
+    if not mats:
+        raise QsgError(11, "InvalidGrid: need a Hamiltonian or collapse operators")
+    d = mats[0].n_rows
+    hc = C.byref(H._c()) if H is not None else None
+    carr = (_Csr * max(1, len(c_ops)))(*[c._c() for c in c_ops]) if len(c_ops) else None
+    return d, hc, carr
+
+
+def liouvillian_export(ctx: "Context", H, c_ops=()) -> CsrMatrix:
+    """L assembled on the device, copied back as host CSR (qsg_liouvillian_export)."""
+    d, hc, carr = _liou_args(H, c_ops)
+    nnz = C.c_int64(0)
+    _check(lib().qsg_liouvillian_export(ctx._h, d, hc, len(c_ops), carr, C.byref(nnz), None, None, None))
+    rp = np.empty(d * d + 1, np.int32)
+    col = np.empty(nnz.value, np.int32)
+    val = np.empty(nnz.value, np.complex128)
+    _check(lib().qsg_liouvillian_export(ctx._h, d, hc, len(c_ops), carr, C.byref(nnz), rp.ctypes.data_as(I32P),
+                                        col.ctypes.data_as(I32P), val.ctypes.data_as(DP)))
+    return CsrMatrix(rp, col, val, d * d, d * d)
+
 
 class Operator:
     """HBM-resident CSR operator (qsg_op)."""
@@ -199,6 +234,12 @@ class Operator:
         c = m._c()
         _check(lib().qsg_op_create(ctx._h, C.byref(c), C.byref(h)))
         self._h, self.ctx, self.n, self.nnz = h, ctx, m.n_rows, m.nnz
+
+    @classmethod
+    def _wrap(cls, ctx, h, n, nnz):
+        o = cls.__new__(cls)
+        o._h, o.ctx, o.n, o.nnz = h, ctx, int(n), int(nnz)
+        return o
 
     def close(self):
         if getattr(self, "_h", None) and _lib is not None:

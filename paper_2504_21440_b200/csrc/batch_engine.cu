@@ -30,6 +30,9 @@ constexpr int kMaxB = 32;       // slots per batch (B = 8 CTA-local, 32 grid-wid
 constexpr int kThreads = 512;   // 16 warps
 constexpr int W = kThreads / 32;
 constexpr int NBUF = 12;
+#ifndef QSG_BATCH_UNROLL
+#define QSG_BATCH_UNROLL 4
+#endif
 #ifndef QSG_BATCH_MINB
 #define QSG_BATCH_MINB 2
 #endif
@@ -173,11 +176,11 @@ __device__ __forceinline__ double2 sell_row_slot(const DevSell& A, int row, XF&&
   double2 acc = make_double2(0.0, 0.0);
   if (A.code_bytes == 0) {
     const long long base = __ldg(A.slice_off + sl) * 32 + ln;
-    for (int j = 0; j < len; j += 4) {
-      int c[4];
-      double2 v[4];
+    for (int j = 0; j < len; j += QSG_BATCH_UNROLL) {
+      int c[QSG_BATCH_UNROLL];
+      double2 v[QSG_BATCH_UNROLL];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < QSG_BATCH_UNROLL; ++u) {
         if (j + u < len) {
           c[u] = __ldg(A.col + base + 32LL * (j + u));
           v[u] = __ldg(A.val + base + 32LL * (j + u));
@@ -187,7 +190,7 @@ __device__ __forceinline__ double2 sell_row_slot(const DevSell& A, int row, XF&&
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < QSG_BATCH_UNROLL; ++u)
         if (j + u < len) cfma(v[u], xf(c[u]), acc);
     }
   } else {
