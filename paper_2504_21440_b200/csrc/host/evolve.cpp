@@ -63,6 +63,7 @@ struct DeviceGenerator {
   std::vector<qsg_coeff> coeffs;
   qsg_generator g{};
 
+  DeviceGenerator() = default;
   DeviceGenerator(qsg_ctx* ctx, const TimeDependentOperator& op, Complex prefactor) {
     add(ctx, (prefactor * op.constant()).sparse_matrix(), qsg_coeff{QSG_COEFF_CONST, 0, 0, 1.0, 0.0});
     for (const auto& t : op.terms()) {
@@ -73,6 +74,17 @@ struct DeviceGenerator {
           qsg_coeff{static_cast<int32_t>(t.coeff.kind()), t.coeff.i(), t.coeff.j(), t.coeff.value().real(),
                     t.coeff.value().imag()});
     }
+    g.n_terms = static_cast<int32_t>(raw.size());
+    g.ops = raw.data();
+    g.coeffs = coeffs.data();
+  }
+  // takes ownership of a store built elsewhere (device Liouvillian assembly)
+  void adopt(qsg_op* op, qsg_coeff c) {
+    auto h = std::make_unique<OpHandle>();
+    h->op = op;
+    raw.push_back(op);
+    ops.push_back(std::move(h));
+    coeffs.push_back(c);
     g.n_terms = static_cast<int32_t>(raw.size());
     g.ops = raw.data();
     g.coeffs = coeffs.data();
@@ -239,7 +251,14 @@ SolveResult mesolve(const TimeDependentOperator& h_or_l, const QuantumObject& rh
                     const SolveOptions& options) {
   check_tlist(tlist);  // evolve.cpp:237-299
   TimeDependentOperator l_td;
-  if (h_or_l.kind() == Kind::Operator) {
+  // An Operator generator with <= 32 collapse operators gets its Liouvillian assembled on the
+  // device (qsg_liouvillian_create, equal to liouvillian() entry for entry); otherwise on the host.
+  const bool device_l = h_or_l.kind() == Kind::Operator && c_ops.size() <= 32;
+  if (device_l) {
+    for (const auto& c : c_ops)  // superop.cpp:87
+      require(c.dims() == h_or_l.dims(), ErrorCode::DimsMismatch, "liouvillian: collapse dims mismatch");
+    l_td = h_or_l;
+  } else if (h_or_l.kind() == Kind::Operator) {
     l_td = liouvillian(h_or_l, c_ops);
   } else {
     require(h_or_l.kind() == Kind::SuperOperator, ErrorCode::KindMismatch,
@@ -255,7 +274,31 @@ SolveResult mesolve(const TimeDependentOperator& h_or_l, const QuantumObject& rh
   const long ne = static_cast<long>(e_ops.size()), nt = static_cast<long>(tlist.size());
   res.expect = DenseMatrix(ne, nt);
   qsg_ctx* ctx = device_ctx(options.device);
-  DeviceGenerator gen(ctx, l_td, Complex(1, 0));
+  DeviceGenerator gen;
+  if (device_l) {
+    const SparseMatrix h0 = h_or_l.constant().sparse_matrix();
+    const qsg_csr hv = csr_view(h0);
+    std::vector<SparseMatrix> cm;
+    for (const auto& c : c_ops) cm.push_back(c.sparse_matrix());
+    std::vector<qsg_csr> cv;
+    for (const auto& m : cm) cv.push_back(csr_view(m));
+    qsg_op* op = nullptr;
+    check(qsg_liouvillian_create(ctx, h_or_l.constant().dim(), &hv, static_cast<int32_t>(cv.size()), cv.data(), &op));
+    gen.adopt(op, qsg_coeff{QSG_COEFF_CONST, 0, 0, 1.0, 0.0});
+    for (const auto& t : h_or_l.terms()) {  // -i(spre(op) - spost(op)) per term (evolve.cpp:39-47)
+      require(t.coeff.kind() != Coeff::Kind::HostOnly, ErrorCode::InvalidGrid,
+              "time-dependent coefficient is a host function; the device solvers accept "
+              "qsim::Coeff::constant/param/param_cos/param_sin");
+      const SparseMatrix tm = t.op.sparse_matrix();
+      const qsg_csr tv = csr_view(tm);
+      qsg_op* top = nullptr;
+      check(qsg_liouvillian_create(ctx, h_or_l.constant().dim(), &tv, 0, nullptr, &top));
+      gen.adopt(top, qsg_coeff{static_cast<int32_t>(t.coeff.kind()), t.coeff.i(), t.coeff.j(),
+                               t.coeff.value().real(), t.coeff.value().imag()});
+    }
+  } else {
+    gen = DeviceGenerator(ctx, l_td, Complex(1, 0));
+  }
   auto e_mats = to_sparse_ops(e_ops, rho0.dims(), "mesolve e_ops");
   std::vector<qsg_csr> ev;
   for (const auto& m : e_mats) ev.push_back(csr_view(m));
