@@ -45,6 +45,10 @@ def lib():
         L.orc_model_psi0.argtypes = [P, DP]
         for f in (L.orc_mesolve, L.orc_sesolve):
             f.argtypes = [P, DP, C.c_int, DP, C.c_int, DP, C.c_int, DP, DP, LP, DP]
+        L.orc_ssesolve.argtypes = [P, DP, C.c_int, DP, C.c_int, C.c_ulonglong, C.c_int, C.c_int, C.c_double,
+                                   C.c_int, DP, DP, DP, DP, DP, LP, DP]
+        L.orc_smesolve.argtypes = [P, C.c_int, DP, C.c_int, DP, C.c_int, C.c_ulonglong, C.c_int, C.c_int,
+                                   C.c_double, C.c_int, DP, DP, DP, DP, DP, LP, DP]
         L.orc_mcsolve.argtypes = [P, DP, C.c_int, DP, C.c_int, DP, C.c_ulonglong, C.c_int, C.c_int,
                                   DP, DP, LP, IP, DP, IP, C.c_int, IP]
         L.orc_generator_apply.argtypes = [P, C.c_int, C.c_double, DP, C.c_int, DP, DP]
@@ -169,6 +173,43 @@ class Model:
         _check(lib().orc_mesolve_prepared(self._h, _dp(t), len(t), _dp(prm), len(prm), _dp(opts),
                                           expect.ctypes.data_as(DP), stats.ctypes.data_as(LP)))
         return expect.reshape(len(t), self.n_eops).T.copy(), stats
+
+    def _sde(self, sme, n_det, tlist, seed, ntraj, dt_max, store_measurement, n_threads, params):
+        t = np.ascontiguousarray(tlist, np.float64)
+        prm = np.ascontiguousarray(self.default_params if params is None else params, np.float64)
+        ne, nt = self.n_eops, len(t)
+        n_ch = self.n_cops - (n_det if sme else 0)
+        mean = np.zeros(ne * nt, np.complex128)
+        per = np.zeros(ntraj * ne * nt, np.complex128)
+        nsteps = C.c_long(0)
+        dt = C.c_double(0)
+        # grid size first (no measurement buffers), then the real run
+        span = t[-1] - t[0]
+        sp = t[1] - t[0]
+        dtm = dt_max if dt_max > 0 else span / 1e4
+        sub = max(1, int(np.ceil(sp / dtm * (1.0 - 1e-12))))
+        n_steps = sub * (nt - 1)
+        w = [np.zeros(ntraj * n_ch * n_steps) for _ in range(3)] if store_measurement else [None] * 3
+        args = (_dp(t), nt, _dp(prm), len(prm), seed, ntraj, n_threads, dt_max, 1 if store_measurement else 0,
+                mean.ctypes.data_as(DP), per.ctypes.data_as(DP), *[_dp(x) for x in w], C.byref(nsteps), C.byref(dt))
+        rc = lib().orc_smesolve(self._h, n_det, *args) if sme else lib().orc_ssesolve(self._h, *args)
+        _check(rc)
+        out = {"mean": mean.reshape(nt, ne).T.copy(),
+               "per_traj": per.reshape(ntraj, nt, ne).transpose(0, 2, 1).copy(),
+               "n_steps": nsteps.value, "dt": dt.value}
+        if store_measurement:
+            sh = lambda x: x.reshape(ntraj, nsteps.value, n_ch).transpose(0, 2, 1).copy()
+            out["increments"], out["expectation"], out["current"] = (sh(x) for x in w)
+        return out
+
+    def ssesolve(self, tlist, seed, ntraj, dt_max=0.0, store_measurement=False, n_threads=0, params=None):
+        """trajectories.cpp:367-393 with every model c_op as a measurement channel."""
+        return self._sde(False, 0, tlist, seed, ntraj, dt_max, store_measurement, n_threads, params)
+
+    def smesolve(self, tlist, seed, ntraj, n_det=0, dt_max=0.0, store_measurement=False, n_threads=0,
+                 params=None):
+        """trajectories.cpp:474-503: model c_ops[:n_det] deterministic, the rest measured."""
+        return self._sde(True, n_det, tlist, seed, ntraj, dt_max, store_measurement, n_threads, params)
 
     def mcsolve(self, tlist, seed, ntraj, n_threads=0, params=None, abstol=1e-8, reltol=1e-6,
                 max_steps=10_000_000, jcap=512):

@@ -248,6 +248,68 @@ int orc_mcsolve(void* hp, const double* tlist, int nt, const double* params, int
   }
 }
 
+/// Stochastic solvers (trajectories.cpp:251-503) on a zoo model. ssesolve: every model c_op is a
+/// measurement channel (sc_op). smesolve: the first n_det model c_ops are deterministic c_ops, the
+/// rest sc_ops. mean: n_e x n_t; per_traj (optional): ntraj x (n_e x n_t) complex;
+/// winc/wexp/wcur (optional, store_measurement): ntraj x (n_ch x n_steps) doubles;
+/// *n_steps_out / *dt_out: the Euler-Maruyama grid.
+static int sde_common(void* hp, int sme, int n_det, const double* tlist, int nt, const double* params, int np,
+                      unsigned long long seed, int ntraj, int nthreads, double dt_max, int store_meas,
+                      double* mean, double* per_traj, double* winc, double* wexp, double* wcur, long* n_steps_out,
+                      double* dt_out) {
+  try {
+    const Model& m = static_cast<Handle*>(hp)->m;
+    Params prm = np > 0 ? Params(params, params + np) : m.params;
+    EnsembleOptions ens;
+    ens.ntraj = ntraj;
+    ens.seed = seed;
+    ens.n_threads = nthreads;
+    ens.dt_max = dt_max;
+    ens.store_measurement = store_meas != 0;
+    std::span<const double> tl(tlist, static_cast<size_t>(nt));
+    EnsembleResult r;
+    if (!sme) {
+      r = ssesolve(m.h, m.psi0, tl, m.c_ops, m.e_ops, ens, prm);
+    } else {
+      const size_t nd = static_cast<size_t>(std::max(0, std::min<int>(n_det, static_cast<int>(m.c_ops.size()))));
+      std::span<const QObj> cops(m.c_ops.data(), nd), scops(m.c_ops.data() + nd, m.c_ops.size() - nd);
+      r = smesolve(m.h, m.psi0, tl, cops, scops, m.e_ops, ens, prm);
+    }
+    write_dense(r.mean_expect, mean);
+    const EmGrid g = make_em_grid(tl, dt_max);
+    if (n_steps_out) *n_steps_out = g.n_steps;
+    if (dt_out) *dt_out = g.dt;
+    const size_t blk = static_cast<size_t>(m.e_ops.size()) * static_cast<size_t>(nt);
+    for (int i = 0; i < ntraj; ++i) {
+      const auto& s = r.raw[static_cast<size_t>(i)];
+      if (per_traj) std::memcpy(per_traj + 2 * blk * static_cast<size_t>(i), s.expect.v.data(), blk * sizeof(cd));
+      if (s.has_wiener) {
+        const size_t w = s.wiener.increments.size();
+        if (winc) std::memcpy(winc + w * static_cast<size_t>(i), s.wiener.increments.data(), w * sizeof(double));
+        if (wexp) std::memcpy(wexp + w * static_cast<size_t>(i), s.wiener.expectation.data(), w * sizeof(double));
+        if (wcur) std::memcpy(wcur + w * static_cast<size_t>(i), s.wiener.current.data(), w * sizeof(double));
+      }
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int orc_ssesolve(void* hp, const double* tlist, int nt, const double* params, int np, unsigned long long seed,
+                 int ntraj, int nthreads, double dt_max, int store_meas, double* mean, double* per_traj,
+                 double* winc, double* wexp, double* wcur, long* n_steps_out, double* dt_out) {
+  return sde_common(hp, 0, 0, tlist, nt, params, np, seed, ntraj, nthreads, dt_max, store_meas, mean, per_traj,
+                    winc, wexp, wcur, n_steps_out, dt_out);
+}
+
+int orc_smesolve(void* hp, int n_det, const double* tlist, int nt, const double* params, int np,
+                 unsigned long long seed, int ntraj, int nthreads, double dt_max, int store_meas, double* mean,
+                 double* per_traj, double* winc, double* wexp, double* wcur, long* n_steps_out, double* dt_out) {
+  return sde_common(hp, 1, n_det, tlist, nt, params, np, seed, ntraj, nthreads, dt_max, store_meas, mean, per_traj,
+                    winc, wexp, wcur, n_steps_out, dt_out);
+}
+
 /// out = G y for the selected generator (which = 4 Liouvillian / 6 mcsolve -iH_eff /
 /// 8 sesolve -iH), including parameter terms at time t.
 int orc_generator_apply(void* hp, int which, double t, const double* params, int np,

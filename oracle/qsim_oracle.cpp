@@ -1118,6 +1118,231 @@ EnsembleResult mcsolve(const TdOp& h, const QObj& psi0, std::span<const double> 
 }
 
 // ======================================================================================
+// stochastic solvers (trajectories.cpp:251-503), every Eigen expression element-wise in order
+// ======================================================================================
+EmGrid make_em_grid(std::span<const double> tlist, double dt_max) {  // trajectories.cpp:261-275
+  const double span = tlist.back() - tlist.front();
+  const double spacing = tlist[1] - tlist[0];
+  for (size_t i = 2; i < tlist.size(); ++i)
+    require(std::abs((tlist[i] - tlist[i - 1]) - spacing) <= 1e-9 * spacing, ErrorCode::InvalidGrid,
+            "stochastic solvers need a uniform tlist");
+  if (dt_max <= 0.0) dt_max = span / 1e4;
+  EmGrid g;
+  g.substeps_per_interval = std::max(1L, static_cast<long>(std::ceil(spacing / dt_max * (1.0 - 1e-12))));
+  g.dt = spacing / static_cast<double>(g.substeps_per_interval);
+  g.n_steps = g.substeps_per_interval * static_cast<long>(tlist.size() - 1);
+  return g;
+}
+
+namespace {
+double vnorm(const Vec& a) { return std::sqrt(sqnorm(a)); }
+
+struct SseSetup {
+  SparseGenerator gen;  // -i H(t)
+  std::vector<Csc> s_mats, sds_mats, x_mats, e_mats;
+};
+
+void init_wiener(TrajectoryData& d, const EmGrid& g, size_t n_ch) {
+  d.has_wiener = true;
+  d.wiener.dt = g.dt;
+  d.wiener.n_ch = static_cast<long>(n_ch);
+  d.wiener.n_steps = g.n_steps;
+  const size_t sz = n_ch * static_cast<size_t>(g.n_steps);
+  d.wiener.increments.assign(sz, 0.0);
+  d.wiener.expectation.assign(sz, 0.0);
+  d.wiener.current.assign(sz, 0.0);
+}
+
+TrajectoryData simulate_sse_trajectory(const SseSetup& setup, const Vec& y0, std::span<const double> tlist,
+                                       const EmGrid& grid, bool store, RngStream& rng) {  // :283-363
+  TrajectoryData data;
+  const long n_e = static_cast<long>(setup.e_mats.size()), n_t = static_cast<long>(tlist.size());
+  const size_t n_ch = setup.s_mats.size(), n = y0.size();
+  data.expect = Dense(n_e, n_t);
+  if (store) init_wiener(data, grid, n_ch);
+  Vec psi = y0, drift(n), tmp(n), stoch(n);
+  std::vector<double> e_vals(n_ch), dw(n_ch);
+  auto observe = [&](long k) {
+    for (long e = 0; e < n_e; ++e) {
+      sp_gemv(setup.e_mats[static_cast<size_t>(e)], psi.data(), tmp.data());
+      data.expect(e, k) = dotc(psi, tmp);
+    }
+  };
+  observe(0);
+  const bool single = n_ch == 1;
+  long step = 0;
+  for (long k = 1; k < n_t; ++k) {
+    for (long s = 0; s < grid.substeps_per_interval; ++s, ++step) {
+      const double t = tlist.front() + grid.dt * static_cast<double>(step);
+      setup.gen.apply(t, psi, drift);
+      if (single) {  // :313-326
+        sp_gemv(setup.x_mats[0], psi.data(), tmp.data());
+        const double e_n = dotc(psi, tmp).real();
+        const double dw0 = std::sqrt(grid.dt) * rng.normal();
+        sp_gemv(setup.s_mats[0], psi.data(), stoch.data());
+        sp_gemv(setup.sds_mats[0], psi.data(), tmp.data());
+        const double c1 = grid.dt * 0.5 * e_n + dw0, c2 = grid.dt * 0.5;
+        const double c3 = grid.dt * 0.125 * e_n * e_n + 0.5 * e_n * dw0;
+        for (size_t i = 0; i < n; ++i)
+          psi[i] = psi[i] + (((grid.dt * drift[i] + c1 * stoch[i]) - c2 * tmp[i]) - c3 * psi[i]);
+        const double nrm = vnorm(psi);
+        for (auto& v : psi) v = v / nrm;
+        e_vals[0] = e_n;
+        dw[0] = dw0;
+      } else {  // :327-347
+        for (auto& v : stoch) v = cd(0.0, 0.0);
+        for (size_t c = 0; c < n_ch; ++c) {
+          sp_gemv(setup.x_mats[c], psi.data(), tmp.data());
+          const double e_n = dotc(psi, tmp).real();
+          e_vals[c] = e_n;
+          dw[c] = std::sqrt(grid.dt) * rng.normal();
+          sp_gemv(setup.s_mats[c], psi.data(), tmp.data());
+          const double a = 0.5 * e_n, b = 0.5 * e_n * dw[c];
+          for (size_t i = 0; i < n; ++i) drift[i] += a * tmp[i];
+          for (size_t i = 0; i < n; ++i) stoch[i] += dw[c] * tmp[i];
+          for (size_t i = 0; i < n; ++i) stoch[i] -= b * psi[i];
+          sp_gemv(setup.sds_mats[c], psi.data(), tmp.data());
+          const double q = 0.125 * e_n * e_n;
+          for (size_t i = 0; i < n; ++i) drift[i] -= 0.5 * tmp[i];
+          for (size_t i = 0; i < n; ++i) drift[i] -= q * psi[i];
+        }
+        for (size_t i = 0; i < n; ++i) psi[i] += grid.dt * drift[i] + stoch[i];
+        const double nrm = vnorm(psi);
+        for (auto& v : psi) v = v / nrm;
+      }
+      if (store)
+        for (size_t c = 0; c < n_ch; ++c) {  // :348-353
+          const size_t idx = c + n_ch * static_cast<size_t>(step);
+          data.wiener.increments[idx] = dw[c];
+          data.wiener.expectation[idx] = e_vals[c];
+          data.wiener.current[idx] = e_vals[c] + dw[c] / grid.dt;
+        }
+    }
+    observe(k);
+  }
+  data.steps = grid.n_steps;
+  data.rhs_evals = grid.n_steps;
+  return data;
+}
+
+struct SmeSetup {
+  SparseGenerator gen;  // full Liouvillian including the sc_op dissipators
+  std::vector<Csc> s_mats, e_mats;
+  long d = 0;
+};
+
+TrajectoryData simulate_sme_trajectory(const SmeSetup& setup, const Vec& rho0, std::span<const double> tlist,
+                                       const EmGrid& grid, bool store, RngStream& rng) {  // :408-470
+  TrajectoryData data;
+  const long n_e = static_cast<long>(setup.e_mats.size()), n_t = static_cast<long>(tlist.size());
+  const size_t n_ch = setup.s_mats.size();
+  const long d = setup.d;
+  const size_t nn = static_cast<size_t>(d * d);
+  data.expect = Dense(n_e, n_t);
+  if (store) init_wiener(data, grid, n_ch);
+  Vec rho = rho0, srho(nn), hop(nn), rho_new(nn), drift(nn);
+  auto at = [&](const Vec& m, long i, long j) -> const cd& { return m[static_cast<size_t>(i + d * j)]; };
+  auto observe = [&](long k) {
+    for (long e = 0; e < n_e; ++e) {
+      cd acc = 0.0;
+      const Csc& a = setup.e_mats[static_cast<size_t>(e)];
+      for (long c = 0; c < a.cols; ++c)
+        for (int p = a.outer[static_cast<size_t>(c)]; p < a.outer[static_cast<size_t>(c + 1)]; ++p)
+          acc += a.val[static_cast<size_t>(p)] * at(rho, c, a.inner[static_cast<size_t>(p)]);
+      data.expect(e, k) = acc;
+    }
+  };
+  observe(0);
+  long step = 0;
+  for (long k = 1; k < n_t; ++k) {
+    for (long s = 0; s < grid.substeps_per_interval; ++s, ++step) {
+      const double t = tlist.front() + grid.dt * static_cast<double>(step);
+      setup.gen.apply(t, rho, drift);
+      for (size_t i = 0; i < nn; ++i) rho_new[i] = rho[i] + grid.dt * drift[i];
+      for (size_t c = 0; c < n_ch; ++c) {
+        for (long j = 0; j < d; ++j)  // S * rho, column by column (sparse x dense product)
+          sp_gemv(setup.s_mats[c], rho.data() + d * j, srho.data() + d * j);
+        for (long j = 0; j < d; ++j)
+          for (long i = 0; i < d; ++i) hop[static_cast<size_t>(i + d * j)] = at(srho, i, j) + std::conj(at(srho, j, i));
+        cd tr = 0.0;
+        for (long i = 0; i < d; ++i) tr += at(hop, i, i);
+        const double e_n = tr.real();
+        const double dw = std::sqrt(grid.dt) * rng.normal();
+        for (size_t i = 0; i < nn; ++i) hop[i] -= e_n * rho[i];
+        for (size_t i = 0; i < nn; ++i) rho_new[i] += dw * hop[i];
+        if (store) {
+          const size_t idx = c + n_ch * static_cast<size_t>(step);
+          data.wiener.increments[idx] = dw;
+          data.wiener.expectation[idx] = e_n;
+          data.wiener.current[idx] = e_n + dw / grid.dt;
+        }
+      }
+      for (long j = 0; j < d; ++j)
+        for (long i = 0; i < d; ++i)
+          rho[static_cast<size_t>(i + d * j)] = 0.5 * (at(rho_new, i, j) + std::conj(at(rho_new, j, i)));
+      cd tr = 0.0;
+      for (long i = 0; i < d; ++i) tr += at(rho, i, i);
+      const double trr = tr.real();
+      for (auto& v : rho) v = v / trr;
+    }
+    observe(k);
+  }
+  data.steps = grid.n_steps;
+  data.rhs_evals = grid.n_steps;
+  return data;
+}
+}  // namespace
+
+EnsembleResult ssesolve(const TdOp& h, const QObj& psi0, std::span<const double> tlist,
+                        std::span<const QObj> sc_ops, std::span<const QObj> e_ops, const EnsembleOptions& ens,
+                        const Params& params) {  // trajectories.cpp:367-393
+  check_tlist(tlist);
+  require(psi0.is_ket(), ErrorCode::KindMismatch, "ssesolve expects a Ket initial state");
+  require(h.constant.kind == Kind::Operator, ErrorCode::KindMismatch, "ssesolve expects an Operator H");
+  require(h.constant.dims == psi0.dims, ErrorCode::DimsMismatch, "H and psi0 dims differ");
+  SseSetup setup{SparseGenerator(h, cd(0, -1), params), {}, {}, {}, {}};
+  for (const auto& s : sc_ops) {
+    require(s.dims == psi0.dims, ErrorCode::DimsMismatch, "sc_op dims mismatch");
+    setup.s_mats.push_back(s.sparse());
+    setup.sds_mats.push_back((dag(s) * s).sparse());
+    setup.x_mats.push_back((s + dag(s)).sparse());
+  }
+  for (const auto& e : e_ops) setup.e_mats.push_back(e.sparse());
+  const EmGrid grid = make_em_grid(tlist, ens.dt_max);
+  Dense p0 = psi0.dense();
+  Vec y0(p0.v.begin(), p0.v.end());
+  const double nrm = vnorm(y0);
+  for (auto& v : y0) v = v / nrm;
+  auto sim = [&](int, RngStream& rng) {
+    return simulate_sse_trajectory(setup, y0, tlist, grid, ens.store_measurement, rng);
+  };
+  return run_ensemble(sim, static_cast<int>(e_ops.size()), tlist, ens);
+}
+
+EnsembleResult smesolve(const TdOp& h, const QObj& rho0_in, std::span<const double> tlist,
+                        std::span<const QObj> c_ops, std::span<const QObj> sc_ops, std::span<const QObj> e_ops,
+                        const EnsembleOptions& ens, const Params& params) {  // trajectories.cpp:474-503
+  check_tlist(tlist);
+  require(h.constant.kind == Kind::Operator, ErrorCode::KindMismatch, "smesolve expects an Operator H");
+  QObj rho0 = rho0_in.is_ket() ? ket2dm(rho0_in) : rho0_in;
+  require(rho0.kind == Kind::Operator, ErrorCode::KindMismatch, "smesolve expects a Ket or Operator state");
+  require(rho0.dims == h.constant.dims, ErrorCode::DimsMismatch, "H and rho0 dims differ");
+  std::vector<QObj> all_ops(c_ops.begin(), c_ops.end());
+  all_ops.insert(all_ops.end(), sc_ops.begin(), sc_ops.end());
+  TdOp l_td = liouvillian_td(h, all_ops);
+  SmeSetup setup{SparseGenerator(l_td, cd(1, 0), params), {}, {}, rho0.dim};
+  for (const auto& s : sc_ops) setup.s_mats.push_back(s.sparse());
+  for (const auto& e : e_ops) setup.e_mats.push_back(e.sparse());
+  const EmGrid grid = make_em_grid(tlist, ens.dt_max);
+  Dense m0 = rho0.dense();
+  Vec r0(m0.v.begin(), m0.v.end());
+  auto sim = [&](int, RngStream& rng) {
+    return simulate_sme_trajectory(setup, r0, tlist, grid, ens.store_measurement, rng);
+  };
+  return run_ensemble(sim, static_cast<int>(e_ops.size()), tlist, ens);
+}
+
+// ======================================================================================
 // model zoo: assembled in reference style (scenario.cpp:247-395, test fixtures)
 // ======================================================================================
 static CoeffFn param_coeff(size_t i) {
@@ -1184,6 +1409,25 @@ Model build_model(const std::string& name, std::span<const double> p) {
     m.psi0 = tensor(fock(n, 0), basis(2, 0));
     if (kappa > 0.0 || gamma > 0.0) m.c_ops = {std::sqrt(kappa) * a, std::sqrt(gamma) * sm};
     m.e_ops = {dag(a) * a, sz};
+  } else if (name == "jc_sse" || name == "jc_sme") {
+    // scenario.cpp:252-277, stochastic solvers: jc_sse (N, wc, wa, g, kappa): c_ops = sc_ops =
+    // {sqrt(kappa) a}; jc_sme (N, wc, wa, g, kappa, gamma, kphi): c_ops = {sqrt(gamma) sm,
+    // sqrt(kphi) a^dag a} (deterministic) followed by the measured sqrt(kappa) a.
+    // e_ops: n_cavity, sz_atom, X_quadrature = sqrt(kappa) (a + a^dag).
+    const int n = static_cast<int>(P(0));
+    const double wc = P(1), wa = P(2), g = P(3), kappa = P(4);
+    QObj a = tensor(destroy(n), qeye(2));
+    QObj sz = tensor(qeye(n), sigmaz());
+    QObj sm = tensor(qeye(n), sigmam());
+    QObj sp = tensor(qeye(n), sigmap());
+    m.h.constant = wc * (dag(a) * a) + (wa / 2.0) * sz + g * (a * sp + dag(a) * sm);
+    m.psi0 = tensor(fock(n, 0), basis(2, 0));
+    if (name == "jc_sse") {
+      m.c_ops = {std::sqrt(kappa) * a};
+    } else {
+      m.c_ops = {std::sqrt(P(5)) * sm, std::sqrt(P(6)) * (dag(a) * a), std::sqrt(kappa) * a};
+    }
+    m.e_ops = {dag(a) * a, sz, std::sqrt(kappa) * (a + dag(a))};
   } else if (name == "damped_cavity") {  // N, omega, gamma, n0 (test_evolve.cpp:124-140)
     const int n = static_cast<int>(P(0));
     QObj a = destroy(n);

@@ -245,6 +245,14 @@ struct EnsembleOptions {
   std::uint64_t seed = 0;
   int n_threads = 0;
   bool store_per_traj = true;
+  bool store_measurement = false;  // trajectories.hpp:31 (stochastic solvers)
+  double dt_max = 0.0;             // trajectories.hpp:32 (<= 0: span / 1e4)
+};
+// Wiener record of one stochastic trajectory (trajectories.hpp:18-24): n_ch x n_steps, col-major.
+struct WienerRecord {
+  double dt = 0.0;
+  long n_ch = 0, n_steps = 0;
+  std::vector<double> increments, expectation, current;
 };
 struct TrajectoryData {
   Dense expect;
@@ -252,6 +260,8 @@ struct TrajectoryData {
   bool failed = false;
   std::string failure;
   long steps = 0, rejected = 0, rhs_evals = 0;
+  bool has_wiener = false;
+  WienerRecord wiener;
 };
 struct EnsembleResult {
   std::vector<double> times;
@@ -271,6 +281,19 @@ EnsembleResult mcsolve(const TdOp& h, const QObj& psi0, std::span<const double> 
                        std::span<const QObj> c_ops, std::span<const QObj> e_ops,
                        const EnsembleOptions& ens, const Params& params,
                        const SolveOptions& opt);
+// Euler-Maruyama stochastic Schroedinger / master equations (trajectories.cpp:251-503)
+struct EmGrid {
+  long substeps_per_interval = 1;
+  double dt = 0.0;
+  long n_steps = 0;
+};
+EmGrid make_em_grid(std::span<const double> tlist, double dt_max);
+EnsembleResult ssesolve(const TdOp& h, const QObj& psi0, std::span<const double> tlist,
+                        std::span<const QObj> sc_ops, std::span<const QObj> e_ops,
+                        const EnsembleOptions& ens, const Params& params);
+EnsembleResult smesolve(const TdOp& h, const QObj& rho0, std::span<const double> tlist,
+                        std::span<const QObj> c_ops, std::span<const QObj> sc_ops,
+                        std::span<const QObj> e_ops, const EnsembleOptions& ens, const Params& params);
 
 // ---- model zoo (scenario.cpp:247-395 style assembly) -------------------------------------
 struct Model {

@@ -86,6 +86,18 @@ qsg_model* build(const std::string& name, const double* p, int np) {
     m->psi0 = tensor(fock(n, 0), basis(2, 0));
     if (kappa > 0.0 || gamma > 0.0) m->c_ops = {std::sqrt(kappa) * a, std::sqrt(gamma) * sm};
     m->e_ops = {dag(a) * a, sz};
+  } else if (name == "jc_sse" || name == "jc_sme") {  // scenario.cpp:252-277 (stochastic solvers)
+    const int n = static_cast<int>(P(0));
+    const double wc = P(1), wa = P(2), g = P(3), kappa = P(4);
+    QuantumObject a = tensor(destroy(n), qeye(2));
+    QuantumObject sz = tensor(qeye(n), sigmaz());
+    QuantumObject sm = tensor(qeye(n), sigmam());
+    QuantumObject sp = tensor(qeye(n), sigmap());
+    m->h = wc * (dag(a) * a) + (wa / 2.0) * sz + g * (a * sp + dag(a) * sm);
+    m->psi0 = tensor(fock(n, 0), basis(2, 0));
+    if (name == "jc_sse") m->c_ops = {std::sqrt(kappa) * a};
+    else m->c_ops = {std::sqrt(P(5)) * sm, std::sqrt(P(6)) * (dag(a) * a), std::sqrt(kappa) * a};
+    m->e_ops = {dag(a) * a, sz, std::sqrt(kappa) * (a + dag(a))};
   } else if (name == "damped_cavity") {
     const int n = static_cast<int>(P(0));
     QuantumObject a = destroy(n);
