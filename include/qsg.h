@@ -167,6 +167,34 @@ qsg_status qsg_sesolve(qsg_ctx* ctx, const qsg_generator* G, int64_t d, const do
                        const double* params, int32_t n_params, const qsg_solve_opts* opts,
                        double* expect, double* states, qsg_stats* stats, qsg_timing* timing);
 
+/* ---- stochastic Schroedinger / master equations (trajectories.cpp:251-503) ------------- */
+typedef struct {
+  double* per_traj_expect; /* optional: n_blk x (n_e x n_t) complex, col-major blocks      */
+  double* block_sum;       /* required: n_e x n_t complex, pairwise sum over the block     */
+  int64_t n_ok;            /* out: trajectories in block_sum                               */
+  double* w_increments;    /* optional (store_measurement): n_blk x (n_ch x n_steps) dW    */
+  double* w_expectation;   /*   e_c per step                                              */
+  double* w_current;       /*   J = e_c + dW / dt (trajectories.hpp:18-24)                */
+  int64_t n_steps;         /* out: Euler-Maruyama steps per trajectory (make_em_grid)    */
+  double dt;               /* out: step size                                              */
+} qsg_sde_out;
+
+/* ssesolve (trajectories.cpp:367-393) for trajectories [traj_begin, traj_end): G = -i H(t),
+ * sc_ops d x d (S^dag S and S + S^dag are formed here in the reference's arithmetic), psi0 is
+ * normalised; tlist must be uniform. Trajectory i uses RngStream(seed, i). At most 8 channels. */
+qsg_status qsg_ssesolve(qsg_ctx* ctx, const qsg_generator* G, int64_t d, int32_t n_sc,
+                        const qsg_csr* sc_ops, int32_t n_e, const qsg_csr* e_ops, const double* psi0,
+                        const double* tlist, int64_t n_t, const double* params, int32_t n_params,
+                        uint64_t seed, int64_t traj_begin, int64_t traj_end, double dt_max,
+                        int32_t store_measurement, qsg_sde_out* out, qsg_timing* timing);
+/* smesolve (trajectories.cpp:474-503): L = the full Liouvillian including the sc_op
+ * dissipators (qsg_liouvillian_create over c_ops followed by sc_ops), rho0 d x d col-major. */
+qsg_status qsg_smesolve(qsg_ctx* ctx, const qsg_generator* L, int64_t d, int32_t n_sc,
+                        const qsg_csr* sc_ops, int32_t n_e, const qsg_csr* e_ops, const double* rho0,
+                        const double* tlist, int64_t n_t, const double* params, int32_t n_params,
+                        uint64_t seed, int64_t traj_begin, int64_t traj_end, double dt_max,
+                        int32_t store_measurement, qsg_sde_out* out, qsg_timing* timing);
+
 /* ---- Monte-Carlo trajectories (trajectories.cpp:106-249) ------------------------------ */
 typedef struct {
   /* outputs, all optional (NULL to skip) except block_sum / n_ok */

@@ -79,6 +79,11 @@ class _McOut(C.Structure):
                 ("jump_time", DP), ("jump_channel", I32P), ("jump_capacity", C.c_int64)]
 
 
+class _SdeOut(C.Structure):
+    _fields_ = [("per_traj_expect", DP), ("block_sum", DP), ("n_ok", C.c_int64), ("w_increments", DP),
+                ("w_expectation", DP), ("w_current", DP), ("n_steps", C.c_int64), ("dt", C.c_double)]
+
+
 def build(verbose: bool = False) -> None:
     """Compile lib/libqsim_b200.so (sm_100a) in-tree."""
     subprocess.run(["make", "-C", _PKG] + ([] if verbose else ["-s"]), check=True)
@@ -115,6 +120,10 @@ def lib():
                                         DP, C.POINTER(_Stats), I32P, C.POINTER(_Timing)]
         L.qsg_rng_draw.argtypes = [P, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, DP,
                                    C.POINTER(C.c_uint64)]
+        for f in (L.qsg_ssesolve, L.qsg_smesolve):
+            f.argtypes = [P, C.POINTER(_Gen), C.c_int64, C.c_int32, C.POINTER(_Csr), C.c_int32, C.POINTER(_Csr),
+                          DP, DP, C.c_int64, DP, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_double,
+                          C.c_int32, C.POINTER(_SdeOut), C.POINTER(_Timing)]
         L.qsg_liouvillian_create.argtypes = [P, C.c_int64, C.POINTER(_Csr), C.c_int32, C.POINTER(_Csr),
                                              C.POINTER(P)]
         L.qsg_liouvillian_export.argtypes = [P, C.c_int64, C.POINTER(_Csr), C.c_int32, C.POINTER(_Csr),
@@ -387,6 +396,50 @@ def mcsolve(ctx: Context, G: Generator, c_ops, e_ops, d: int, psi0, tlist, seed:
         "attempts": tm.attempts,
         "grid_ctas": tm.grid_ctas,
     }
+
+
+def _em_steps(t, dt_max):
+    span, sp = t[-1] - t[0], t[1] - t[0]
+    dtm = dt_max if dt_max > 0 else span / 1e4
+    return max(1, int(np.ceil(sp / dtm * (1.0 - 1e-12)))) * (len(t) - 1)
+
+
+def _sde(fn, ctx, G, sc_ops, e_ops, d, y0, tlist, seed, traj_begin, traj_end, dt_max, store_measurement, params):
+    t = np.ascontiguousarray(tlist, np.float64)
+    prm = None if params is None else np.ascontiguousarray(params, np.float64)
+    ne, nt, nb, nch = len(e_ops), len(t), traj_end - traj_begin, len(sc_ops)
+    per = np.zeros(nb * ne * nt, np.complex128)
+    bsum = np.zeros(max(1, ne * nt), np.complex128)
+    nst = _em_steps(t, dt_max)
+    w = [np.zeros(nb * nch * nst) for _ in range(3)] if store_measurement and nch else [None] * 3
+    out = _SdeOut(_dp(per), _dp(bsum), 0, _dp(w[0]), _dp(w[1]), _dp(w[2]), 0, 0.0)
+    tm = _Timing()
+    y = np.ascontiguousarray(y0, np.complex128)
+    _check(fn(ctx._h, C.byref(G._g), d, nch, _csr_array(sc_ops), ne, _csr_array(e_ops), _dp(y), _dp(t), nt,
+              _dp(prm), 0 if prm is None else len(prm), seed, traj_begin, traj_end, dt_max,
+              1 if store_measurement else 0, C.byref(out), C.byref(tm)))
+    bs = bsum[: ne * nt].reshape(nt, ne).T.copy()
+    res = {"per_traj": per.reshape(nb, nt, ne).transpose(0, 2, 1).copy(), "block_sum": bs, "n_ok": out.n_ok,
+           "mean": ensemble_combine([(0, nb)], [bs], out.n_ok) if ne else bs, "n_steps": out.n_steps,
+           "dt": out.dt, "kernel_ms": tm.kernel_ms, "grid_ctas": tm.grid_ctas}
+    if w[0] is not None:
+        sh = lambda x: x.reshape(nb, out.n_steps, nch).transpose(0, 2, 1).copy()
+        res["increments"], res["expectation"], res["current"] = (sh(x) for x in w)
+    return res
+
+
+def ssesolve(ctx: Context, G: Generator, sc_ops, e_ops, d: int, psi0, tlist, seed: int, traj_begin: int,
+             traj_end: int, dt_max=0.0, store_measurement=False, params=None):
+    """qsg_ssesolve: Euler-Maruyama SSE trajectories traj_begin..traj_end-1, G = -iH(t)."""
+    return _sde(lib().qsg_ssesolve, ctx, G, sc_ops, e_ops, d, psi0, tlist, seed, traj_begin, traj_end, dt_max,
+                store_measurement, params)
+
+
+def smesolve(ctx: Context, L: Generator, sc_ops, e_ops, d: int, rho0, tlist, seed: int, traj_begin: int,
+             traj_end: int, dt_max=0.0, store_measurement=False, params=None):
+    """qsg_smesolve: L includes the dissipators of c_ops and sc_ops; rho0 column-stacked d x d."""
+    return _sde(lib().qsg_smesolve, ctx, L, sc_ops, e_ops, d, rho0, tlist, seed, traj_begin, traj_end, dt_max,
+                store_measurement, params)
 
 
 def ensemble_combine(block_ranges, block_sums, n_ok_total):
