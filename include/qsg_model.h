@@ -64,6 +64,20 @@ qsg_status qsg_model_mcsolve(qsg_model* m, int32_t n_devices, const int32_t* dev
                              int32_t ntraj, const qsg_solve_opts* opts, double* mean, double* per_traj,
                              int64_t* traj_stats, int32_t* n_jumps, double* jump_time, int32_t* jump_channel,
                              int32_t jump_cap, int32_t* n_failed, double* device_ms);
+/* qsim::ssesolve (every model c_op is a measurement channel, as the reference scenario's
+ * "ssesolve" jc assembly) / qsim::smesolve (model c_ops[0:n_det) unmonitored, the rest measured).
+ * mean: n_e x n_t; per_traj (optional): ntraj x n_e x n_t; w_* (optional, store_measurement):
+ * ntraj x (n_ch x n_steps); *n_steps / *dt: the Euler-Maruyama grid. */
+qsg_status qsg_model_ssesolve(qsg_model* m, int32_t device, const double* tlist, int64_t n_t,
+                              const double* params, int32_t n_params, uint64_t seed, int32_t ntraj,
+                              double dt_max, int32_t store_measurement, double* mean, double* per_traj,
+                              double* w_increments, double* w_expectation, double* w_current,
+                              int64_t* n_steps, double* dt, double* device_ms);
+qsg_status qsg_model_smesolve(qsg_model* m, int32_t device, int32_t n_det, const double* tlist,
+                              int64_t n_t, const double* params, int32_t n_params, uint64_t seed,
+                              int32_t ntraj, double dt_max, int32_t store_measurement, double* mean,
+                              double* per_traj, double* w_increments, double* w_expectation,
+                              double* w_current, int64_t* n_steps, double* dt, double* device_ms);
 
 #ifdef __cplusplus
 }

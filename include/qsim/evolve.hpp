@@ -123,11 +123,23 @@ struct EnsembleOptions {
   std::vector<int> devices;     // GPUs to shard trajectories over (empty: SolveOptions::device)
 };
 
+/// Per-trajectory continuous-measurement record on the Euler-Maruyama grid (trajectories.hpp:18-24).
+/// Eigen::MatrixXd there; here column-major n_channels x n_steps arrays of doubles.
+struct WienerRecord {
+  double dt = 0.0;
+  long n_channels = 0, n_steps = 0;
+  std::vector<double> increments;   // dW_n(t_k)
+  std::vector<double> expectation;  // e_n(t_k) on the pre-step state
+  std::vector<double> current;      // J_n(t_k) = expectation + increments / dt
+  double at(const std::vector<double>& m, long n, long k) const { return m[static_cast<size_t>(n + n_channels * k)]; }
+};
+
 struct TrajectoryEnsembleResult {
   std::vector<double> times;
   DenseMatrix mean_expect;
   std::vector<DenseMatrix> per_traj_expect;
   std::vector<std::vector<JumpEvent>> jump_records;
+  std::vector<WienerRecord> measurement;
   std::vector<int> traj_indices;
   int ntraj = 0;
   std::uint64_t master_seed = 0;
@@ -142,6 +154,21 @@ TrajectoryEnsembleResult mcsolve(const TimeDependentOperator& h, const QuantumOb
                                  std::span<const double> tlist, std::span<const QuantumObject> c_ops,
                                  std::span<const QuantumObject> e_ops, const EnsembleOptions& ens = {},
                                  const Params& params = {}, const SolveOptions& options = {});
+
+/// Homodyne stochastic Schroedinger equation, Euler-Maruyama in Ito form, state renormalised after
+/// every step (trajectories.cpp:367-393); tlist must be uniform. Runs on the device.
+TrajectoryEnsembleResult ssesolve(const TimeDependentOperator& h, const QuantumObject& psi0,
+                                  std::span<const double> tlist, std::span<const QuantumObject> sc_ops,
+                                  std::span<const QuantumObject> e_ops, const EnsembleOptions& ens = {},
+                                  const Params& params = {}, const SolveOptions& options = {});
+
+/// Homodyne stochastic master equation; c_ops are unmonitored loss channels (trajectories.cpp:474-503).
+/// The Liouvillian over c_ops followed by sc_ops is assembled on the device.
+TrajectoryEnsembleResult smesolve(const TimeDependentOperator& h, const QuantumObject& rho0,
+                                  std::span<const double> tlist, std::span<const QuantumObject> c_ops,
+                                  std::span<const QuantumObject> sc_ops, std::span<const QuantumObject> e_ops,
+                                  const EnsembleOptions& ens = {}, const Params& params = {},
+                                  const SolveOptions& options = {});
 
 // ---- rng.hpp (host copy, for re-deriving thresholds as the reference tests do) -----------------
 class RngStream {

@@ -503,6 +503,10 @@ def _bind_model_api(L):
     L.qsg_model_default_params.argtypes = [P, DP]
     for f in (L.qsg_model_mesolve, L.qsg_model_sesolve):
         f.argtypes = [P, C.c_int32, DP, C.c_int64, DP, C.c_int32, C.POINTER(_Opts), DP, I64P, DP]
+    L.qsg_model_ssesolve.argtypes = [P, C.c_int32, DP, C.c_int64, DP, C.c_int32, C.c_uint64, C.c_int32,
+                                     C.c_double, C.c_int32, DP, DP, DP, DP, DP, I64P, DP, DP]
+    L.qsg_model_smesolve.argtypes = [P, C.c_int32, C.c_int32, DP, C.c_int64, DP, C.c_int32, C.c_uint64,
+                                     C.c_int32, C.c_double, C.c_int32, DP, DP, DP, DP, DP, I64P, DP, DP]
     L.qsg_model_mcsolve.argtypes = [P, C.c_int32, I32P, DP, C.c_int64, DP, C.c_int32, C.c_uint64, C.c_int32,
                                     C.POINTER(_Opts), DP, DP, I64P, I32P, DP, I32P, C.c_int32, I32P, DP]
 
@@ -574,6 +578,40 @@ class Model:
 
     def sesolve(self, tlist, params=None, device=0, abstol=1e-8, reltol=1e-6, max_steps=10_000_000):
         return self._solve(lib().qsg_model_sesolve, device, tlist, params, abstol, reltol, max_steps)
+
+    def _sde(self, sme, n_det, tlist, seed, ntraj, dt_max, store_measurement, device, params):
+        t = np.ascontiguousarray(tlist, np.float64)
+        prm = np.ascontiguousarray(self.default_params if params is None else params, np.float64)
+        ne, nt = self.n_eops, len(t)
+        nch = self.n_cops - (n_det if sme else 0)
+        mean = np.zeros(ne * nt, np.complex128)
+        per = np.zeros(ntraj * ne * nt, np.complex128)
+        nst = _em_steps(t, dt_max)
+        w = [np.zeros(ntraj * nch * nst) for _ in range(3)] if store_measurement and nch else [None] * 3
+        ns = C.c_int64(0)
+        dt = C.c_double(0)
+        ms = C.c_double(0)
+        tail = (_dp(t), len(t), _dp(prm), len(prm), seed, ntraj, dt_max, 1 if store_measurement else 0, _dp(mean),
+                _dp(per), *[_dp(x) for x in w], C.byref(ns), C.byref(dt), C.byref(ms))
+        if sme:
+            _check(lib().qsg_model_smesolve(self._h, device, n_det, *tail))
+        else:
+            _check(lib().qsg_model_ssesolve(self._h, device, *tail))
+        out = {"mean": mean.reshape(nt, ne).T.copy(), "per_traj": per.reshape(ntraj, nt, ne).transpose(0, 2, 1).copy(),
+               "device_ms": ms.value}
+        if w[0] is not None:
+            sh = lambda x: x.reshape(ntraj, ns.value, nch).transpose(0, 2, 1).copy()
+            out["increments"], out["expectation"], out["current"] = (sh(x) for x in w)
+            out["dt"] = dt.value
+        return out
+
+    def ssesolve(self, tlist, seed, ntraj, dt_max=0.0, store_measurement=False, device=0, params=None):
+        """qsim::ssesolve with every model c_op as a measurement channel (trajectories.cpp:367-393)."""
+        return self._sde(False, 0, tlist, seed, ntraj, dt_max, store_measurement, device, params)
+
+    def smesolve(self, tlist, seed, ntraj, n_det=0, dt_max=0.0, store_measurement=False, device=0, params=None):
+        """qsim::smesolve: model c_ops[:n_det] unmonitored, the rest measured (trajectories.cpp:474-503)."""
+        return self._sde(True, n_det, tlist, seed, ntraj, dt_max, store_measurement, device, params)
 
     def mcsolve(self, tlist, seed, ntraj, devices=(0,), params=None, abstol=1e-8, reltol=1e-6,
                 max_steps=10_000_000, jump_cap=256):

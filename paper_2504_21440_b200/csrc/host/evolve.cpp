@@ -457,6 +457,137 @@ TrajectoryEnsembleResult mcsolve(const TimeDependentOperator& h, const QuantumOb
   return r;
 }
 
+namespace {
+// shared tail of ssesolve / smesolve: one device call over [0, ntraj), then the run_ensemble
+// bookkeeping (trajectories.cpp:60-91) and the measurement records
+TrajectoryEnsembleResult run_sde_host(bool sme, qsg_ctx* ctx, const qsg_generator* g, long d,
+                                      std::span<const QuantumObject> sc_ops, std::span<const QuantumObject> e_ops,
+                                      const DenseMatrix& y0, std::span<const double> tlist, const EnsembleOptions& ens,
+                                      const Params& params) {
+  require(ens.ntraj >= 1, ErrorCode::InvalidGrid, "ntraj must be >= 1");
+  std::vector<SparseMatrix> s_mats, e_mats;
+  for (const auto& sop : sc_ops) s_mats.push_back(sop.sparse_matrix());
+  for (const auto& e : e_ops) e_mats.push_back(e.sparse_matrix());
+  std::vector<qsg_csr> sv, ev;
+  for (const auto& m : s_mats) sv.push_back(csr_view(m));
+  for (const auto& m : e_mats) ev.push_back(csr_view(m));
+  const long ne = static_cast<long>(e_ops.size()), nt = static_cast<long>(tlist.size()), ntraj = ens.ntraj;
+  const long blk = ne * nt, nch = static_cast<long>(sc_ops.size());
+  // Euler-Maruyama grid size for the record buffers (make_em_grid, trajectories.cpp:261-275)
+  const double span = tlist.back() - tlist.front(), spacing = tlist[1] - tlist[0];
+  const double dtm = ens.dt_max <= 0.0 ? span / 1e4 : ens.dt_max;
+  const long n_steps = std::max(1L, static_cast<long>(std::ceil(spacing / dtm * (1.0 - 1e-12)))) * (nt - 1);
+  std::vector<Complex> per(static_cast<size_t>(ntraj * blk)), bsum(static_cast<size_t>(std::max<long>(1, blk)));
+  const bool rec = ens.store_measurement && nch > 0;
+  std::vector<double> wi, we, wc;
+  if (rec) {
+    wi.resize(static_cast<size_t>(ntraj * nch * n_steps));
+    we.resize(wi.size());
+    wc.resize(wi.size());
+  }
+  qsg_sde_out out{};
+  out.per_traj_expect = reinterpret_cast<double*>(per.data());
+  out.block_sum = reinterpret_cast<double*>(bsum.data());
+  out.w_increments = rec ? wi.data() : nullptr;
+  out.w_expectation = rec ? we.data() : nullptr;
+  out.w_current = rec ? wc.data() : nullptr;
+  qsg_timing tm{};
+  auto fn = sme ? qsg_smesolve : qsg_ssesolve;
+  check(fn(ctx, g, d, static_cast<int32_t>(nch), sv.data(), static_cast<int32_t>(ne), ev.data(),
+           reinterpret_cast<const double*>(y0.data()), tlist.data(), nt, params.data(),
+           static_cast<int32_t>(params.size()), ens.seed, 0, ntraj, ens.dt_max, rec ? 1 : 0, &out, &tm));
+  TrajectoryEnsembleResult r;
+  r.times.assign(tlist.begin(), tlist.end());
+  r.ntraj = static_cast<int>(ntraj);
+  r.master_seed = ens.seed;
+  r.device_ms = tm.kernel_ms;
+  std::vector<DenseMatrix> mats(static_cast<size_t>(ntraj));
+  std::vector<const DenseMatrix*> ok;
+  for (long i = 0; i < ntraj; ++i) {
+    DenseMatrix m(ne, nt);
+    std::copy(per.begin() + i * blk, per.begin() + (i + 1) * blk, m.data());
+    mats[static_cast<size_t>(i)] = std::move(m);
+    ok.push_back(&mats[static_cast<size_t>(i)]);
+    r.traj_indices.push_back(static_cast<int>(i));
+    r.stats.steps += out.n_steps;      // ode_stats.steps = rhs_evals = n_steps (:359-360)
+    r.stats.rhs_evals += out.n_steps;
+  }
+  r.mean_expect = pairwise_sum(ok, 0, ok.size());
+  for (long i = 0; i < r.mean_expect.size(); ++i)
+    r.mean_expect.data()[i] = r.mean_expect.data()[i] / Complex(static_cast<double>(ok.size()), 0.0);
+  for (long i = 0; i < ntraj; ++i) {
+    r.jump_records.emplace_back();
+    if (ens.store_per_traj) r.per_traj_expect.push_back(mats[static_cast<size_t>(i)]);
+    if (rec) {
+      WienerRecord w;
+      w.dt = out.dt;
+      w.n_channels = nch;
+      w.n_steps = out.n_steps;
+      const size_t o = static_cast<size_t>(i * nch * out.n_steps), len = static_cast<size_t>(nch * out.n_steps);
+      w.increments.assign(wi.begin() + o, wi.begin() + o + len);
+      w.expectation.assign(we.begin() + o, we.begin() + o + len);
+      w.current.assign(wc.begin() + o, wc.begin() + o + len);
+      r.measurement.push_back(std::move(w));
+    }
+  }
+  return r;
+}
+}  // namespace
+
+TrajectoryEnsembleResult ssesolve(const TimeDependentOperator& h, const QuantumObject& psi0,
+                                  std::span<const double> tlist, std::span<const QuantumObject> sc_ops,
+                                  std::span<const QuantumObject> e_ops, const EnsembleOptions& ens,
+                                  const Params& params, const SolveOptions& options) {
+  check_tlist(tlist);  // trajectories.cpp:367-393
+  require(psi0.is_ket(), ErrorCode::KindMismatch, "ssesolve expects a Ket initial state");
+  require(h.kind() == Kind::Operator, ErrorCode::KindMismatch, "ssesolve expects an Operator H");
+  require(h.dims() == psi0.dims(), ErrorCode::DimsMismatch, "H and psi0 dims differ");
+  for (const auto& s : sc_ops) require(s.dims() == psi0.dims(), ErrorCode::DimsMismatch, "sc_op dims mismatch");
+  qsg_ctx* ctx = device_ctx(ens.devices.empty() ? options.device : ens.devices.front());
+  DeviceGenerator gen(ctx, h, Complex(0, -1));
+  return run_sde_host(false, ctx, &gen.g, psi0.dim(), sc_ops, e_ops, psi0.dense_matrix(), tlist, ens, params);
+}
+
+TrajectoryEnsembleResult smesolve(const TimeDependentOperator& h, const QuantumObject& rho0_in,
+                                  std::span<const double> tlist, std::span<const QuantumObject> c_ops,
+                                  std::span<const QuantumObject> sc_ops, std::span<const QuantumObject> e_ops,
+                                  const EnsembleOptions& ens, const Params& params, const SolveOptions& options) {
+  check_tlist(tlist);  // trajectories.cpp:474-503
+  require(h.kind() == Kind::Operator, ErrorCode::KindMismatch, "smesolve expects an Operator H");
+  QuantumObject rho0 = rho0_in.is_ket() ? ket2dm(rho0_in) : rho0_in;
+  require(rho0.is_operator(), ErrorCode::KindMismatch, "smesolve expects a Ket or Operator state");
+  require(rho0.dims() == h.dims(), ErrorCode::DimsMismatch, "H and rho0 dims differ");
+  std::vector<QuantumObject> all_ops(c_ops.begin(), c_ops.end());
+  all_ops.insert(all_ops.end(), sc_ops.begin(), sc_ops.end());
+  for (const auto& c : all_ops)
+    require(c.dims() == h.dims(), ErrorCode::DimsMismatch, "liouvillian: collapse dims mismatch");
+  require(all_ops.size() <= 32, ErrorCode::TooLarge, "smesolve supports at most 32 channels");
+  qsg_ctx* ctx = device_ctx(ens.devices.empty() ? options.device : ens.devices.front());
+  // L = liouvillian(h, c_ops + sc_ops) assembled on the device, td terms as in mesolve
+  DeviceGenerator gen;
+  const SparseMatrix h0 = h.constant().sparse_matrix();
+  const qsg_csr hv = csr_view(h0);
+  std::vector<SparseMatrix> cm;
+  for (const auto& c : all_ops) cm.push_back(c.sparse_matrix());
+  std::vector<qsg_csr> cv;
+  for (const auto& m : cm) cv.push_back(csr_view(m));
+  qsg_op* op = nullptr;
+  check(qsg_liouvillian_create(ctx, h.constant().dim(), &hv, static_cast<int32_t>(cv.size()), cv.data(), &op));
+  gen.adopt(op, qsg_coeff{QSG_COEFF_CONST, 0, 0, 1.0, 0.0});
+  for (const auto& t : h.terms()) {
+    require(t.coeff.kind() != Coeff::Kind::HostOnly, ErrorCode::InvalidGrid,
+            "time-dependent coefficient is a host function; the device solvers accept "
+            "qsim::Coeff::constant/param/param_cos/param_sin");
+    const SparseMatrix tm = t.op.sparse_matrix();
+    const qsg_csr tv = csr_view(tm);
+    qsg_op* top = nullptr;
+    check(qsg_liouvillian_create(ctx, h.constant().dim(), &tv, 0, nullptr, &top));
+    gen.adopt(top, qsg_coeff{static_cast<int32_t>(t.coeff.kind()), t.coeff.i(), t.coeff.j(), t.coeff.value().real(),
+                             t.coeff.value().imag()});
+  }
+  return run_sde_host(true, ctx, &gen.g, rho0.dim(), sc_ops, e_ops, rho0.dense_matrix(), tlist, ens, params);
+}
+
 std::vector<double> ensemble_stddev(const TrajectoryEnsembleResult& r) {  // trajectories.cpp:94-104
   require(!r.per_traj_expect.empty(), ErrorCode::InvalidGrid, "per-trajectory data was not stored");
   const size_t sz = static_cast<size_t>(r.mean_expect.size());

@@ -288,4 +288,62 @@ qsg_status qsg_model_mcsolve(qsg_model* m, int32_t n_devices, const int32_t* dev
   }
 }
 
+static qsg_status model_sde(qsg_model* m, bool sme, int32_t device, int32_t n_det, const double* tlist, int64_t n_t,
+                            const double* params, int32_t n_params, uint64_t seed, int32_t ntraj, double dt_max,
+                            int32_t store, double* mean, double* per_traj, double* wi, double* we, double* wc,
+                            int64_t* n_steps, double* dt, double* device_ms) {
+  try {
+    SolveOptions o;
+    o.device = device;
+    EnsembleOptions ens;
+    ens.ntraj = ntraj;
+    ens.seed = seed;
+    ens.dt_max = dt_max;
+    ens.store_measurement = store != 0;
+    Params prm = n_params > 0 ? Params(params, params + n_params) : m->params;
+    std::span<const double> tl(tlist, static_cast<size_t>(n_t));
+    TrajectoryEnsembleResult r;
+    if (!sme) {
+      r = ssesolve(m->h, m->psi0, tl, m->c_ops, m->e_ops, ens, prm, o);
+    } else {
+      const size_t nd = static_cast<size_t>(std::clamp<int32_t>(n_det, 0, static_cast<int32_t>(m->c_ops.size())));
+      std::span<const QuantumObject> all(m->c_ops);
+      r = smesolve(m->h, m->psi0, tl, all.subspan(0, nd), all.subspan(nd), m->e_ops, ens, prm, o);
+    }
+    if (mean) std::memcpy(mean, r.mean_expect.data(), static_cast<size_t>(r.mean_expect.size()) * sizeof(Complex));
+    const size_t blk = static_cast<size_t>(r.mean_expect.size());
+    for (size_t i = 0; i < r.per_traj_expect.size(); ++i)
+      if (per_traj) std::memcpy(per_traj + 2 * blk * i, r.per_traj_expect[i].data(), blk * sizeof(Complex));
+    for (size_t i = 0; i < r.measurement.size(); ++i) {
+      const auto& w = r.measurement[i];
+      const size_t len = w.increments.size();
+      if (wi) std::memcpy(wi + len * i, w.increments.data(), len * sizeof(double));
+      if (we) std::memcpy(we + len * i, w.expectation.data(), len * sizeof(double));
+      if (wc) std::memcpy(wc + len * i, w.current.data(), len * sizeof(double));
+      if (n_steps) *n_steps = w.n_steps;
+      if (dt) *dt = w.dt;
+    }
+    if (device_ms) *device_ms = r.device_ms;
+    return QSG_OK;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+qsg_status qsg_model_ssesolve(qsg_model* m, int32_t device, const double* tlist, int64_t n_t, const double* params,
+                              int32_t n_params, uint64_t seed, int32_t ntraj, double dt_max, int32_t store,
+                              double* mean, double* per_traj, double* wi, double* we, double* wc, int64_t* n_steps,
+                              double* dt, double* device_ms) {
+  return model_sde(m, false, device, 0, tlist, n_t, params, n_params, seed, ntraj, dt_max, store, mean, per_traj, wi,
+                   we, wc, n_steps, dt, device_ms);
+}
+
+qsg_status qsg_model_smesolve(qsg_model* m, int32_t device, int32_t n_det, const double* tlist, int64_t n_t,
+                              const double* params, int32_t n_params, uint64_t seed, int32_t ntraj, double dt_max,
+                              int32_t store, double* mean, double* per_traj, double* wi, double* we, double* wc,
+                              int64_t* n_steps, double* dt, double* device_ms) {
+  return model_sde(m, true, device, n_det, tlist, n_t, params, n_params, seed, ntraj, dt_max, store, mean, per_traj,
+                   wi, we, wc, n_steps, dt, device_ms);
+}
+
 }  // extern "C"

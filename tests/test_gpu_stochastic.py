@@ -76,3 +76,18 @@ def test_sse_ensemble_matches_oracle_and_converges(ctx):
     assert normwise_rel(dev["mean"], ref["mean"]) <= TOL
     me, _, _ = m.mesolve(t)
     assert np.max(np.abs(dev["mean"][2] - me[2])) < 0.25
+
+
+def test_cpp_ssesolve_smesolve_match_oracle():
+    """qsim::ssesolve / qsim::smesolve of the C++ host API (zoo models) against the oracle."""
+    t = np.linspace(0.0, 0.5, 6)
+    dev = q.Model("jc_sse", 6, 1.0, 1.0, 0.1, 0.3).ssesolve(t, 31, 8, dt_max=1e-3, store_measurement=True)
+    ref = O.Model("jc_sse", 6, 1.0, 1.0, 0.1, 0.3).ssesolve(t, 31, 8, dt_max=1e-3, store_measurement=True)
+    assert normwise_rel(dev["mean"], ref["mean"]) <= TOL
+    assert np.max(np.abs(dev["increments"] - ref["increments"])) <= 1e-13 * np.max(np.abs(ref["increments"]))
+    prm = (4, 1.0, 1.0, 0.1, 1.0, 0.1, 0.05)
+    t2 = np.linspace(0.0, 1.0, 11)
+    dev = q.Model("jc_sme", *prm).smesolve(t2, 7, 6, n_det=2, dt_max=2e-3)
+    ref = O.Model("jc_sme", *prm).smesolve(t2, 7, 6, n_det=2, dt_max=2e-3)
+    for i in range(6):
+        assert normwise_rel(dev["per_traj"][i], ref["per_traj"][i]) <= TOL, i

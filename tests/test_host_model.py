@@ -16,6 +16,8 @@ MODELS = [
     ("ising", (2, 2, 0.9, 0.4, 0.2, 1)),
     ("ising", (5, 1, 1.0, 0.2, 1.0, 0)),
     ("jc", (6, 1.0, 1.0, 0.1, 0.01, 0.01)),
+    ("jc_sse", (6, 1.0, 1.0, 0.1, 0.3)),
+    ("jc_sme", (5, 1.0, 1.0, 0.2, 0.4, 0.2, 0.1)),
     ("damped_cavity", (10, 1.0, 0.1, 3)),
     ("decay2", (0.25,)),
     ("driven_cavity_td", (14, 0.4)),
