@@ -274,6 +274,7 @@ def run_ours(args, ws, rank, local):
         secondary["kerr_cutoff_mesolve"] = kerr_cutoff_mesolve(ctx, q, peak)
         secondary["mcsolve"] = mcsolve_sharded(args, ctx, q, torch, ws, rank)
         secondary["param_sweep"] = param_sweep_sharded(args, ctx, q, torch, ws, rank)
+        secondary["stochastic"] = stochastic_secondary(args, q, rank)
     del out, y
 
     line = {
@@ -393,6 +394,34 @@ def param_sweep_sharded(args, ctx, q, torch, ws, rank):
             "failed": int((r["status"] != 0).sum())}
 
 
+def stochastic_secondary(args, q, rank):
+    """ssesolve / smesolve (Euler-Maruyama, trajectories.cpp:251-503) on the
+    reference scenario's JC assembly (scenario.cpp:252-277), N=10, tlist linspace(0,10,101),
+    dt_max 1e-3 (10^4 steps per trajectory). Device time of the trajectory kernel; the oracle
+    (CPU restatement, 1 thread) timed on a few trajectories beside it, rank 0 only."""
+    t = np.linspace(0.0, 10.0, 101)
+    out = {}
+    cases = [("ssesolve", "jc_sse", (10, 1.0, 1.0, 0.1, 0.5), args.sde_traj, False),
+             ("smesolve", "jc_sme", (10, 1.0, 1.0, 0.1, 0.5, 0.1, 0.05), max(1, args.sde_traj // 10), True)]
+    for key, name, prm, ntraj, sme in cases:
+        m = q.Model(name, *prm)
+        run = (lambda n: m.smesolve(t, 5, n, n_det=2, dt_max=1e-3)) if sme else \
+              (lambda n: m.ssesolve(t, 5, n, dt_max=1e-3))
+        run(8)
+        r = run(ntraj)
+        out[key] = {"workload": f"{name}{prm} x {ntraj} trajectories, 10^4 Euler-Maruyama steps each",
+                    "device_s": r["device_ms"] / 1e3, "traj_per_s": ntraj / (r["device_ms"] / 1e3)}
+        if rank == 0:
+            from oracle import oracle as O
+            om = O.Model(name, *prm)
+            k = 2 if sme else 8
+            t0 = time.perf_counter()
+            (om.smesolve(t, 5, k, n_det=2, dt_max=1e-3, n_threads=1) if sme
+             else om.ssesolve(t, 5, k, dt_max=1e-3, n_threads=1))
+            out[key]["cpu_oracle_traj_per_s_1_thread"] = k / (time.perf_counter() - t0)
+    return out
+
+
 def mcsolve_sharded(args, ctx, q, torch, ws, rank):
     """BASELINE configs[2] workload (TFIM-14 mcsolve) on a bounded trajectory count, sharded in
     contiguous blocks (trajectory i = RngStream(2025, i) on every N), NCCL all-gather of block sums."""
@@ -478,6 +507,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mc-traj", type=int, default=10000)
+    ap.add_argument("--sde-traj", type=int, default=2000)
     ap.add_argument("--quick", action="store_true", help="headline only (no secondary workloads)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
