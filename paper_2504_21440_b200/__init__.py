@@ -86,7 +86,8 @@ class _SdeOut(C.Structure):
 
 def build(verbose: bool = False) -> None:
     """Compile lib/libqsim_b200.so (sm_100a) in-tree."""
-    subprocess.run(["make", "-C", _PKG] + ([] if verbose else ["-s"]), check=True)
+    subprocess.run(["make", "-j", str(max(1, os.cpu_count() or 1)), "-C", _PKG] + ([] if verbose else ["-s"]),
+                   check=True)
 
 
 def lib():
