@@ -35,6 +35,7 @@ struct DevSell {
   const unsigned short* code16;
   const int* dict_off;
   const double2* dict_val;
+  int dict_n;  // dictionary entries (0 when plain)
 };
 
 struct DevCoeff {
@@ -159,6 +160,45 @@ __device__ __forceinline__ CodedView coded_view(const DevSell& A) {
   __builtin_assume(__isGlobal(v.dval));
   __builtin_assume(__isGlobal(v.doff));
   return v;
+}
+
+// Coded row with the dictionary staged in shared memory (sval / soff point into __shared__).
+template <class XF>
+__device__ __forceinline__ double2 sell_row_coded_smem(const CodedView& A, const double2* sval, const int* soff,
+                                                       int row, int len, long long base, XF&& xf) {
+  __builtin_assume(__isShared(sval));
+  __builtin_assume(__isShared(soff));
+  double2 acc = make_double2(0.0, 0.0);
+  for (int j0 = 0; j0 < len; j0 += 32) {
+    uint4 w[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + 8 * c;
+      if (j < len) {
+        if (A.cbytes == 1) {
+          const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + j));
+          w[c] = make_uint4(v.x, v.y, 0u, 0u);
+        } else {
+          w[c] = ld_stream_u4(reinterpret_cast<const uint4*>(A.code16 + base + j));
+        }
+      } else {
+        w[c] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + 8 * c + u;
+        if (j < len) {
+          unsigned k;
+          if (A.cbytes == 1) k = ((u < 4 ? w[c].x : w[c].y) >> (8 * (u & 3))) & 0xffu;
+          else k = ((u < 2 ? w[c].x : u < 4 ? w[c].y : u < 6 ? w[c].z : w[c].w) >> (16 * (u & 1))) & 0xffffu;
+          cfma(sval[k], xf(row + soff[k]), acc);
+        }
+      }
+  }
+  return acc;
 }
 
 // Coded row through a CodedView: `len` entries whose codes start at offset `base`.

@@ -181,7 +181,8 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 }
 
 template <int S, bool PF>
-__device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c, int s0, int s1) {
+__device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c, int s0, int s1,
+                                             const double2* sval = nullptr, const int* soff = nullptr) {
   using namespace dp;
   const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = P.n;
@@ -287,7 +288,8 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
         const bool ok = row < n;
         Ops o;
         load_operands(row, ok, o);
-        const double2 k = sell_row_coded_v(cv, row, len, base, xin);
+        const double2 k = sval ? sell_row_coded_smem(cv, sval, soff, row, len, base, xin)
+                               : sell_row_coded_v(cv, row, len, base, xin);
         if (bn < s1) {
           const char* cp = cv.cbytes == 1 ? reinterpret_cast<const char*>(cv.code8 + base_n)
                                           : reinterpret_cast<const char*>(cv.code16 + base_n);
@@ -438,6 +440,7 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
   __shared__ double s_red[kThreads / 32];
   __shared__ double s_val[2];
   __shared__ Ctl c;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
 
   const int G = gridDim.x, rank = blockIdx.x;
   const int nsl = (P.n + 31) >> 5;
@@ -473,6 +476,22 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
       push_pending(P, c, __longlong_as_double(0x7ff8000000000000ll));
   }
   __syncthreads();
+
+  // dictionary of a single-term coded generator staged in shared memory (P.smem_dict entries)
+  const double2* sval = nullptr;
+  const int* soff = nullptr;
+  if (PF && P.smem_dict > 0) {
+    const DevSell& A = P.gen.A[0];
+    double2* dv = reinterpret_cast<double2*>(s_dyn);
+    int* dof = reinterpret_cast<int*>(dv + P.smem_dict);
+    for (int i = threadIdx.x; i < P.smem_dict; i += blockDim.x) {
+      dv[i] = A.dict_val[i];
+      dof[i] = A.dict_off[i];
+    }
+    __syncthreads();
+    sval = dv;
+    soff = dof;
+  }
 
   // ---------------- start + initial_step ----------------
   {
@@ -534,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     __syncthreads();
     if (c.done || c.status != kRunning) break;
     // stage 2 (+ observations of the previous accepted step)
-    stage_pass<2, PF>(P, c, s0, s1);
+    stage_pass<2, PF>(P, c, s0, s1, sval, soff);
     if (c.np) observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
     grid_barrier(P.bar, G);
     if (c.np) {
@@ -545,15 +564,15 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
         c.np = 0;
       }
     }
-    stage_pass<3, PF>(P, c, s0, s1);
+    stage_pass<3, PF>(P, c, s0, s1, sval, soff);
     grid_barrier(P.bar, G);
-    stage_pass<4, PF>(P, c, s0, s1);
+    stage_pass<4, PF>(P, c, s0, s1, sval, soff);
     grid_barrier(P.bar, G);
-    stage_pass<5, PF>(P, c, s0, s1);
+    stage_pass<5, PF>(P, c, s0, s1, sval, soff);
     grid_barrier(P.bar, G);
-    stage_pass<6, PF>(P, c, s0, s1);
+    stage_pass<6, PF>(P, c, s0, s1, sval, soff);
     grid_barrier(P.bar, G);
-    double esq = stage_pass<7, PF>(P, c, s0, s1);
+    double esq = stage_pass<7, PF>(P, c, s0, s1, sval, soff);
     esq = block_sum(esq, s_red);
     if (threadIdx.x == 0) red[static_cast<long long>(kSlotErr) * G + rank] = esq;
     grid_barrier(P.bar, G);
@@ -598,17 +617,21 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
   }
 }
 
+size_t dict_smem_bytes(const GridProblem& P) {
+  return static_cast<size_t>(P.smem_dict) * (sizeof(double2) + sizeof(int));
+}
+
 template <int MODE, bool PF>
 cudaError_t launch_one(const GridProblem& P, int grid, cudaStream_t s) {
   void* args[] = {const_cast<GridProblem*>(&P)};
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dp5_grid_kernel<MODE, PF>), dim3(grid),
-                                     dim3(kThreads), args, 0, s);
+                                     dim3(kThreads), args, dict_smem_bytes(P), s);
 }
 
 template <int MODE, bool PF>
-int occupancy_one() {
+int occupancy_one(size_t smem) {
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp5_grid_kernel<MODE, PF>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp5_grid_kernel<MODE, PF>, kThreads, smem);
   return nb;
 }
 
@@ -616,9 +639,9 @@ int occupancy_one() {
 
 int grid_threads() { return kThreads; }
 
-int grid_max_blocks_per_sm(int mode, bool pf) {
-  if (mode == 0) return pf ? occupancy_one<0, true>() : occupancy_one<0, false>();
-  return pf ? occupancy_one<1, true>() : occupancy_one<1, false>();
+int grid_max_blocks_per_sm(int mode, bool pf, size_t dyn_smem) {
+  if (mode == 0) return pf ? occupancy_one<0, true>(dyn_smem) : occupancy_one<0, false>(dyn_smem);
+  return pf ? occupancy_one<1, true>(dyn_smem) : occupancy_one<1, false>(dyn_smem);
 }
 
 cudaError_t launch_grid_dp5(const GridProblem& P, int mode, bool pf, int grid, cudaStream_t s) {

@@ -20,6 +20,7 @@ struct GridCtl {
 };
 
 struct GridProblem {
+  int smem_dict;  // > 0: the single-term coded generator's dictionary (entries) staged in shared memory
   int n;     // vector length (d*d for mesolve, d for sesolve)
   int d;     // Hilbert dimension
   DevGen gen;
@@ -51,7 +52,7 @@ struct GridProblem {
 };
 
 int grid_threads();
-int grid_max_blocks_per_sm(int mode, bool pf);
+int grid_max_blocks_per_sm(int mode, bool pf, size_t dyn_smem = 0);
 cudaError_t launch_grid_dp5(const GridProblem& P, int mode, bool pf, int grid, cudaStream_t s);
 
 }  // namespace qsg

@@ -54,6 +54,7 @@ DevSell sell_view(const qsg_op* op, bool use_codes) {
   v.code16 = op->code_bytes == 2 ? static_cast<const unsigned short*>(op->code) : nullptr;
   v.dict_off = op->dict_off;
   v.dict_val = op->dict_val;
+  v.dict_n = op->dict_n;
   return v;
 }
 
@@ -545,7 +546,13 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   const int threads = grid_threads();
   bool pf = true;  // prefetching stage variant when every term uses the coded store
   for (int k = 0; k < G->n_terms; ++k) pf = pf && G->ops[k]->code_bytes > 0;
-  const int per_sm = grid_max_blocks_per_sm(mode, pf);
+  // Stage a single-term coded generator's dictionary (<= 2048 entries) in shared memory: its lookups
+  // then cost shared-memory wavefronts instead of L1 ones (QSG_SMEM_DICT=0 disables).
+  const char* sd = std::getenv("QSG_SMEM_DICT");
+  if (pf && G->n_terms == 1 && G->ops[0]->dict_n > 0 && G->ops[0]->dict_n <= 2048 && !(sd && sd[0] == '0'))
+    P.smem_dict = G->ops[0]->dict_n;
+  const size_t dyn = static_cast<size_t>(P.smem_dict) * (sizeof(double2) + sizeof(int));
+  const int per_sm = grid_max_blocks_per_sm(mode, pf, dyn);
   if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "occupancy");
   const int max_grid = per_sm * ctx->sm_count;
   const long long nblk = (n + 31) / 32;
