@@ -195,15 +195,14 @@ __device__ __forceinline__ double2 sell_row_slot(const DevSell& A, int row, XF&&
     }
   } else {
     const long long cb = __ldg(A.code_off + sl);
-    const int wp = static_cast<int>((__ldg(A.code_off + sl + 1) - cb) >> 5);
-    const long long base = cb + static_cast<long long>(ln) * wp;
+    const long long base = cb + 8LL * ln;  // interleaved groups of 8 codes (qsg_capi.cu)
     for (int j = 0; j < len; j += 8) {
       uint4 w;
       if (A.code_bytes == 1) {
-        const uint2 v = __ldg(reinterpret_cast<const uint2*>(A.code8 + base + j));
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(A.code8 + base + 32LL * j));
         w = make_uint4(v.x, v.y, 0u, 0u);
       } else {
-        w = __ldg(reinterpret_cast<const uint4*>(A.code16 + base + j));
+        w = __ldg(reinterpret_cast<const uint4*>(A.code16 + base + 32LL * j));
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)

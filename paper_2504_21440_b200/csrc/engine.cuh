@@ -176,10 +176,10 @@ __device__ __forceinline__ double2 sell_row_coded_smem(const CodedView& A, const
       const int j = j0 + 8 * c;
       if (j < len) {
         if (A.cbytes == 1) {
-          const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + j));
+          const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + 32LL * j));
           w[c] = make_uint4(v.x, v.y, 0u, 0u);
         } else {
-          w[c] = ld_stream_u4(reinterpret_cast<const uint4*>(A.code16 + base + j));
+          w[c] = ld_stream_u4(reinterpret_cast<const uint4*>(A.code16 + base + 32LL * j));
         }
       } else {
         w[c] = make_uint4(0u, 0u, 0u, 0u);
@@ -212,10 +212,10 @@ __device__ __forceinline__ double2 sell_row_coded_v(const CodedView& A, int row,
       const int j = j0 + 8 * c;
       if (j < len) {
         if (A.cbytes == 1) {
-          const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + j));
+          const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + 32LL * j));
           w[c] = make_uint4(v.x, v.y, 0u, 0u);
         } else {
-          w[c] = ld_stream_u4(reinterpret_cast<const uint4*>(A.code16 + base + j));
+          w[c] = ld_stream_u4(reinterpret_cast<const uint4*>(A.code16 + base + 32LL * j));
         }
       } else {
         w[c] = make_uint4(0u, 0u, 0u, 0u);
@@ -237,9 +237,11 @@ __device__ __forceinline__ double2 sell_row_coded_v(const CodedView& A, int row,
   return acc;
 }
 
-// Coded-store row with its metadata already loaded: `len` entries whose codes start at byte (or
-// uint16) offset `base`. The row's codes are contiguous (a multiple of 8 per row), so 8 codes come
-// in one 8 B (uint8) or 16 B (uint16) load and a 32-entry row is in flight after 4 loads.
+// Coded-store row with its metadata already loaded: `len` entries whose first group of 8 codes
+// starts at entry `base` = code_off[slice] + 8 * lane. Codes are interleaved in groups of 8 entries
+// (group g of the slice's 32 rows is one contiguous 256-entry run), so 8 codes come in one 8 B
+// (uint8) or 16 B (uint16) load, a warp's load is one contiguous 256 / 512 B request, and a
+// 32-entry row is in flight after 4 loads.
 template <class XF>
 __device__ __forceinline__ double2 sell_row_coded(const DevSell& A, int row, int len, long long base, XF&& xf) {
   double2 acc = make_double2(0.0, 0.0);
@@ -250,10 +252,10 @@ __device__ __forceinline__ double2 sell_row_coded(const DevSell& A, int row, int
       const int j = j0 + 8 * c;
       if (j < len) {
         if (A.code_bytes == 1) {
-          const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + j));
+          const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + 32LL * j));
           w[c] = make_uint4(v.x, v.y, 0u, 0u);
         } else {
-          w[c] = ld_stream_u4(reinterpret_cast<const uint4*>(A.code16 + base + j));
+          w[c] = ld_stream_u4(reinterpret_cast<const uint4*>(A.code16 + base + 32LL * j));
         }
       } else {
         w[c] = make_uint4(0u, 0u, 0u, 0u);
@@ -300,9 +302,7 @@ __device__ __forceinline__ double2 sell_row(const DevSell& A, int slice, int lan
         if (j + u < len) cfma(v[u], xf(c[u]), acc);
     }
   } else {
-    const long long cb = __ldg(A.code_off + slice);
-    const int wp = static_cast<int>((__ldg(A.code_off + slice + 1) - cb) >> 5);
-    acc = sell_row_coded(A, row, len, cb + static_cast<long long>(lane) * wp, xf);
+    acc = sell_row_coded(A, row, len, __ldg(A.code_off + slice) + 8LL * lane, xf);
   }
   return acc;
 }

@@ -272,9 +272,7 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
       const long long* __restrict__ code_off = A.code_off;
       auto meta = [&](int b, int& len, long long& base) {
         len = __ldg(rowlen + b * 32 + lane);
-        const long long cb = __ldg(code_off + b);
-        const int wp = static_cast<int>((__ldg(code_off + b + 1) - cb) >> 5);
-        base = cb + static_cast<long long>(lane) * wp;
+        base = __ldg(code_off + b) + 8LL * lane;  // interleaved groups of 8 codes
       };
       int b = s0 + warp, len = 0;
       long long base = 0;
@@ -291,10 +289,11 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
         const double2 k = sval ? sell_row_coded_smem(cv, sval, soff, row, len, base, xin)
                                : sell_row_coded_v(cv, row, len, base, xin);
         if (bn < s1) {
-          const char* cp = cv.cbytes == 1 ? reinterpret_cast<const char*>(cv.code8 + base_n)
-                                          : reinterpret_cast<const char*>(cv.code16 + base_n);
-          prefetch_l2(cp);
-          if (len_n * cv.cbytes > 32) prefetch_l2(cp + len_n * cv.cbytes - 1);
+          // the next slice's code block (32 rows x width codes, contiguous): one sector run per lane
+          const long long cb_n = base_n - 8LL * lane;
+          const char* blk = cv.cbytes == 1 ? reinterpret_cast<const char*>(cv.code8 + cb_n)
+                                           : reinterpret_cast<const char*>(cv.code16 + cb_n);
+          prefetch_l2(blk + lane * 32 * cv.cbytes);  // 1 KB x code bytes window (array padded by 1 K codes)
           const int rn = (bn << 5) + lane;
           if (rn < n) {
             prefetch_l2(y + rn);

@@ -213,18 +213,6 @@ __global__ void sell_fill_kernel(const int* rowptr, const int* col, const double
   }
 }
 
-// codes of row r at code_off[slice] + (r % 32) * Wp + k, Wp = slice width rounded up to 8
-template <class T>
-__global__ void sell_code_fill_kernel(const int* rowptr, const T* codes, int n, const long long* code_off, T* scode) {
-  const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const int b = rowptr[r], e = rowptr[r + 1];
-  const long long cb = code_off[r >> 5];
-  const long long wp = (code_off[(r >> 5) + 1] - cb) >> 5;
-  const long long base = cb + (r & 31) * wp;
-  for (int k = 0; k < e - b; ++k) scode[base + k] = codes[b + k];
-}
-
 // ---- dictionary of distinct (column - row, value) pairs, built on the device -------------------
 // Lock-free open addressing: a 64-bit signature claims a slot by CAS, the owner then publishes the
 // full key; equal signatures are confirmed against the full key (exact bit patterns), so the
@@ -315,10 +303,10 @@ __global__ void sell_code_fill_dense_kernel(const int* rowptr, const unsigned* s
   const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int b = rowptr[r], e = rowptr[r + 1];
-  const long long cb = code_off[r >> 5];
-  const long long wp = (code_off[(r >> 5) + 1] - cb) >> 5;
-  const long long base = cb + (r & 31) * wp;
-  for (int k = 0; k < e - b; ++k) scode[base + k] = static_cast<T>(dense[slot_of[b + k]]);
+  // interleaved groups of 8 entries: entry k of lane l at code_off[slice] + (k/8)*256 + 8*l + k%8, so
+  // a warp's 8-code loads of one group are one contiguous 256-entry run
+  const long long base = code_off[r >> 5] + (r & 31) * 8;
+  for (int k = 0; k < e - b; ++k) scode[base + (k >> 3) * 256 + (k & 7)] = static_cast<T>(dense[slot_of[b + k]]);
 }
 
 // Builds the coded store of `op` from the staged CSR; leaves op plain when the operator has more
@@ -352,7 +340,8 @@ static cudaError_t build_coded_store(qsg_op* op, const int* rp, const int* col, 
   const int cbytes = count <= 256 ? 1 : 2;
   std::vector<long long> coff(nsl + 1, 0);
   for (long long i = 0; i < nsl; ++i) coff[i + 1] = coff[i] + 32 * ((w[i] + 7) / 8 * 8);
-  const size_t pc = static_cast<size_t>(std::max<long long>(1, coff[nsl]));
+  // + 1024 codes of tail padding: the grid engine prefetches a 1 K-code window per slice
+  const size_t pc = static_cast<size_t>(std::max<long long>(1, coff[nsl])) + 1024;
   if ((e = cudaMallocAsync(&op->code, pc * cbytes, s)) ||
       (e = cudaMallocAsync(&op->code_off, sizeof(long long) * (nsl + 1), s)) ||
       (e = cudaMallocAsync(&op->dict_off, sizeof(int) * count, s)) ||
