@@ -321,6 +321,14 @@ __device__ __forceinline__ double2 gen_row(const DevGen& g, const double* params
   return s;
 }
 
+// Coherent global load that does not allocate in L1 (streamed operands written by earlier passes
+// of the same kernel; keeps L1 for the x-gathers).
+__device__ __forceinline__ double2 ld_na_c2(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
 // ---- block reduction (deterministic order) ----------------------------------------------------
 // Returns the block total on every thread. smem needs blockDim/32 doubles.
 __device__ __forceinline__ double block_sum(double v, double* smem) {

@@ -213,15 +213,17 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
   struct Ops {
     double2 yy, q1, q2, q3, q4, q5, q6, y1;
   };
+  // streamed once per pass: do not allocate in L1, which then keeps more of the x-gather lines
+  auto ldo = [](const double2* p) { return ld_na_c2(p); };
   auto load_operands = [&](int row, bool ok, Ops& o) {
-    o.yy = ok ? y[row] : z;
-    o.q1 = ok ? k1[row] : z;
-    o.q2 = (S >= 3 && S <= 5 && ok) ? pk2[row] : z;
-    o.q3 = (S >= 4 && ok) ? pk3[row] : z;
-    o.q4 = (S >= 5 && ok) ? pk4[row] : z;
-    o.q5 = (S >= 6 && ok) ? pk5[row] : z;
-    o.q6 = (S == 7 && ok) ? pk6[row] : z;
-    o.y1 = (S == 7 && ok) ? x[row] : z;
+    o.yy = ok ? ldo(y + row) : z;
+    o.q1 = ok ? ldo(k1 + row) : z;
+    o.q2 = (S >= 3 && S <= 5 && ok) ? ldo(pk2 + row) : z;
+    o.q3 = (S >= 4 && ok) ? ldo(pk3 + row) : z;
+    o.q4 = (S >= 5 && ok) ? ldo(pk4 + row) : z;
+    o.q5 = (S >= 6 && ok) ? ldo(pk5 + row) : z;
+    o.q6 = (S == 7 && ok) ? ldo(pk6 + row) : z;
+    o.y1 = (S == 7 && ok) ? ldo(x + row) : z;
   };
   auto xin = [&](int col) {
     if constexpr (S == 2) {
