@@ -228,6 +228,10 @@ __device__ __forceinline__ double2 gen_row_slot(const DevGen& g, const double* p
   return s;
 }
 
+__device__ __forceinline__ void prefetch_row(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -355,6 +359,18 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
   int pub_par = 0;
   auto rows = [&](auto&& f) {
     for (int r = r_lo + warp * RPW + rs; r < r_hi; r += W * RPW) f(r);
+  };
+  // RUN stages: the epilogue operands of this lane's next row (logical buffers in `mask`) are
+  // prefetched into L2 while the current row's SpMV chain is in flight
+  auto rows_pf = [&](unsigned mask, auto&& f) {
+    const int step = W * RPW;
+    for (int r = r_lo + warp * RPW + rs; r < r_hi; r += step) {
+      const int rn = r + step;
+      if (rn < r_hi)
+        for (int k = 0; k < NBUF; ++k)
+          if ((mask >> k) & 1u) prefetch_row(C.buf(k, sl) + static_cast<long long>(rn) * BS + sl);
+      f(r);
+    }
   };
   auto pass_sync = [&]() {
     if constexpr (GRID) grid_barrier(P.bar, gridDim.x);
@@ -484,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       } else if (ph == RUN) {
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
-        rows([&](int r) {
+        rows_pf((1u << Y) | (1u << K1), [&](int r) {
           const double2 k = gen_row_slot(P.gen, prm, r, t + c2 * hh, [&](int c) {
             const double2 a = C.ld(Y, c, sl), q = C.ld(K1, c, sl);
             return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
@@ -644,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       } else if (ph2 == RUN) {
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
-        rows([&](int r) {
+        rows_pf((1u << Y) | (1u << K1) | (1u << K2), [&](int r) {
           const double2 k = gen_row_slot(P.gen, prm, r, t + c3 * hh, [&](int c) { return C.ld(SA, c, sl); });
           const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl);
           C.st(K3, r, sl, k);
@@ -684,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       if (ph3 == RUN) {
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
-        rows([&](int r) {
+        rows_pf((1u << Y) | (1u << K1) | (1u << K2) | (1u << K3), [&](int r) {
           const double2 k = gen_row_slot(P.gen, prm, r, t + c4 * hh, [&](int c) { return C.ld(SB, c, sl); });
           const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl), q3 = C.ld(K3, r, sl);
           C.st(K4, r, sl, k);
@@ -725,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       const double* prm = slot_params(P, S[sl]);
       const double hh = S[sl].hh, t = S[sl].t;
       using namespace dp;
-      rows([&](int r) {
+      rows_pf((1u << Y) | (1u << K1) | (1u << K2) | (1u << K3) | (1u << K4), [&](int r) {
         const double2 k = gen_row_slot(P.gen, prm, r, t + c5 * hh, [&](int c) { return C.ld(SA, c, sl); });
         const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl), q3 = C.ld(K3, r, sl),
                       q4 = C.ld(K4, r, sl);
@@ -740,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       const double* prm = slot_params(P, S[sl]);
       const double hh = S[sl].hh, t = S[sl].t;
       using namespace dp;
-      rows([&](int r) {
+      rows_pf((1u << Y) | (1u << K1) | (1u << K3) | (1u << K4) | (1u << K5), [&](int r) {
         const double2 k = gen_row_slot(P.gen, prm, r, t + hh, [&](int c) { return C.ld(SB, c, sl); });
         const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q3 = C.ld(K3, r, sl), q4 = C.ld(K4, r, sl),
                       q5 = C.ld(K5, r, sl);
@@ -759,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         const double* prm = slot_params(P, S[sl]);
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
-        rows([&](int r) {
+        rows_pf((1u << Y) | (1u << Y1) | (1u << K1) | (1u << K3) | (1u << K4) | (1u << K5) | (1u << K6), [&](int r) {
           const double2 k = gen_row_slot(P.gen, prm, r, t + hh, [&](int c) { return C.ld(Y1, c, sl); });
           const double2 yy = C.ld(Y, r, sl), y1 = C.ld(Y1, r, sl), q1 = C.ld(K1, r, sl), q3 = C.ld(K3, r, sl),
                         q4 = C.ld(K4, r, sl), q5 = C.ld(K5, r, sl), q6 = C.ld(K6, r, sl);
