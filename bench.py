@@ -275,6 +275,7 @@ def run_ours(args, ws, rank, local):
         secondary["mcsolve"] = mcsolve_sharded(args, ctx, q, torch, ws, rank)
         secondary["param_sweep"] = param_sweep_sharded(args, ctx, q, torch, ws, rank)
         secondary["stochastic"] = stochastic_secondary(args, q, rank)
+        secondary["sesolve_tfim20"] = sesolve_tfim20(ctx, q, peak)
     del out, y
 
     line = {
@@ -365,6 +366,32 @@ def kerr_cutoff_mesolve(ctx, q, peak):
         out[f"N{N}"] = {"rows": n, "nnz": nnz, "solve_ms": r["kernel_ms"], "attempts": r["attempts"],
                         "us_per_attempt": r["kernel_ms"] * 1e3 / r["attempts"], "GBps_model": b / r["kernel_ms"] / 1e6,
                         "grid_ctas": r["grid_ctas"], "note": "L2-resident operator: GB/s can exceed the HBM rate"}
+    return out
+
+
+def sesolve_tfim20(ctx, q, peak):
+    """§8a8 sesolve on the same persistent grid engine: closed TFIM chain of 20 spins (ket of
+    1,048,576 amplitudes, G = -iH with 22.0 M entries), all-up start, tlist linspace(0,10,100),
+    Sx/Sy/Sz totals. Device time per solve and the SURVEY §8d byte model of the fused attempt."""
+    t0 = time.perf_counter()
+    m = q.Model("ising", 20, 1, 1.0, 0.2, 0.0, 1)
+    G = m.export(q.SEL_SE_GEN)
+    eops = [m.export(q.SEL_E_OP, k) for k in range(m.n_eops)]
+    host_s = time.perf_counter() - t0
+    op = ctx.op(G)
+    g = q.Generator([op])
+    psi = m.psi0()
+    tl = np.linspace(0.0, 10.0, 100)
+    q.sesolve(ctx, g, m.dim, psi, tl, eops)
+    r = q.sesolve(ctx, g, m.dim, psi, tl, eops)
+    n, nnz = G.n_rows, G.nnz
+    cb, nd = q.op_storage(op)
+    b = (6 * store_bytes(cb, nd, n, nnz) + 47 * 16 * n) * r["attempts"]
+    out = {"workload": "sesolve closed TFIM chain, 20 spins, periodic (ket dim 2^20)", "rows": n, "nnz": nnz,
+           "solve_ms": r["kernel_ms"], "attempts": r["attempts"], "store": "coded" if cb else "plain",
+           "dict_pairs": nd, "GBps_model": b / r["kernel_ms"] / 1e6, "frac": b / r["kernel_ms"] / 1e6 / peak,
+           "host_operator_build_s": host_s, "stats_steps_rejected_rhs": list(r["stats"])}
+    op.close()
     return out
 
 
