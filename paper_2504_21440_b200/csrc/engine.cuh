@@ -359,8 +359,20 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
 }
 
 // bar[0] = arrival count, bar[1] = generation. All CTAs of the grid participate.
+#ifdef QSG_BAR_TIMING  // development build: total ns CTAs spend waiting in grid barriers
+static __device__ unsigned long long g_bar_wait_ns, g_bar_calls, g_bar_cta_ns[1024];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 __device__ __forceinline__ void grid_barrier(unsigned* bar, int G) {
   __syncthreads();
+#ifdef QSG_BAR_TIMING
+  const unsigned long long t_in = threadIdx.x == 0 ? gtimer() : 0ull;
+#endif
   if (G > 1 && threadIdx.x == 0) {
     const unsigned gen = ld_acquire_gpu(bar + 1);
     __threadfence();
@@ -375,6 +387,14 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int G) {
     }
     __threadfence();
   }
+#ifdef QSG_BAR_TIMING
+  if (threadIdx.x == 0) {
+    const unsigned long long dt = gtimer() - t_in;
+    atomicAdd(&g_bar_wait_ns, dt);
+    atomicAdd(&g_bar_calls, 1ull);
+    if (blockIdx.x < 1024) g_bar_cta_ns[blockIdx.x] += dt;
+  }
+#endif
   __syncthreads();
 }
 

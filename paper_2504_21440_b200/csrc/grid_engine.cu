@@ -655,3 +655,19 @@ cudaError_t launch_grid_dp5(const GridProblem& P, int mode, bool pf, int grid, c
 }
 
 }  // namespace qsg
+
+#ifdef QSG_BAR_TIMING
+extern "C" void qsg_debug_barrier_ns(unsigned long long* wait_ns, unsigned long long* calls, int reset,
+                                     unsigned long long* per_cta) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(wait_ns, qsg::g_bar_wait_ns, sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(calls, qsg::g_bar_calls, sizeof(unsigned long long));
+  if (per_cta) cudaMemcpyFromSymbol(per_cta, qsg::g_bar_cta_ns, sizeof(unsigned long long) * 1024);
+  if (reset) {
+    static const unsigned long long z[1024] = {};
+    cudaMemcpyToSymbol(qsg::g_bar_wait_ns, z, sizeof(unsigned long long));
+    cudaMemcpyToSymbol(qsg::g_bar_calls, z, sizeof(unsigned long long));
+    cudaMemcpyToSymbol(qsg::g_bar_cta_ns, z, sizeof(z));
+  }
+}
+#endif
