@@ -14,6 +14,7 @@
 // Observations at every tlist point (psi.dot(E psi) :304-309; sum E(r,c) rho(c,r) :429-437).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -478,12 +479,21 @@ qsg_status run_sde(qsg_ctx* ctx, int mode, const qsg_generator* G, int64_t d, in
     P.wexp = d_we.as<double>();
     P.wcur = d_wc.as<double>();
   }
-  const bool small = n <= 256;  // measured: JC N=10 SSE (n = 20) 3.6x faster with one warp, SME (n = 400) 4x slower
-  const int threads = small ? 32 : kSdeThreads;
-  const void* kfn = mode == 0 ? (small ? reinterpret_cast<const void*>(sde_kernel<0, 32>)
-                                       : reinterpret_cast<const void*>(sde_kernel<0, kSdeThreads>))
-                              : (small ? reinterpret_cast<const void*>(sde_kernel<1, 32>)
-                                       : reinterpret_cast<const void*>(sde_kernel<1, kSdeThreads>));
+  // threads per trajectory, measured on JC N=10 (scripts/probe_sde.py): SSE (n = 20) one warp
+  // 35.2k traj/s vs 9.8k at 256 threads; SME (n = 400) 512 threads 3.43k vs 2.83k at 256, 0.70k at 32
+  int threads = n <= 256 ? 32 : 512;
+  if (const char* e = std::getenv("QSG_SDE_THREADS")) {
+    const int v = std::atoi(e);
+    threads = v == 32 || v == 128 || v == 512 ? v : kSdeThreads;
+  }
+  const void* kfn = mode == 0 ? (threads == 32    ? reinterpret_cast<const void*>(sde_kernel<0, 32>)
+                                 : threads == 128 ? reinterpret_cast<const void*>(sde_kernel<0, 128>)
+                                 : threads == 512 ? reinterpret_cast<const void*>(sde_kernel<0, 512>)
+                                                  : reinterpret_cast<const void*>(sde_kernel<0, kSdeThreads>))
+                              : (threads == 32    ? reinterpret_cast<const void*>(sde_kernel<1, 32>)
+                                 : threads == 128 ? reinterpret_cast<const void*>(sde_kernel<1, 128>)
+                                 : threads == 512 ? reinterpret_cast<const void*>(sde_kernel<1, 512>)
+                                                  : reinterpret_cast<const void*>(sde_kernel<1, kSdeThreads>));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, threads, 0);
   if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "occupancy");
@@ -515,9 +525,13 @@ qsg_status run_sde(qsg_ctx* ctx, int mode, const qsg_generator* G, int64_t d, in
   P.queue = d_q.as<unsigned long long>();
   P.expect = d_ex.as<double2>();
   cudaEventRecord(ctx->ev[2], s);
-  if (mode == 0 && small) sde_kernel<0, 32><<<grid, 32, 0, s>>>(P);
+  if (mode == 0 && threads == 32) sde_kernel<0, 32><<<grid, 32, 0, s>>>(P);
+  else if (mode == 0 && threads == 128) sde_kernel<0, 128><<<grid, 128, 0, s>>>(P);
+  else if (mode == 0 && threads == 512) sde_kernel<0, 512><<<grid, 512, 0, s>>>(P);
   else if (mode == 0) sde_kernel<0, kSdeThreads><<<grid, kSdeThreads, 0, s>>>(P);
-  else if (small) sde_kernel<1, 32><<<grid, 32, 0, s>>>(P);
+  else if (threads == 32) sde_kernel<1, 32><<<grid, 32, 0, s>>>(P);
+  else if (threads == 128) sde_kernel<1, 128><<<grid, 128, 0, s>>>(P);
+  else if (threads == 512) sde_kernel<1, 512><<<grid, 512, 0, s>>>(P);
   else sde_kernel<1, kSdeThreads><<<grid, kSdeThreads, 0, s>>>(P);
   if ((ce = cudaGetLastError())) return cuda_fail(ce, "stochastic launch");
   cudaEventRecord(ctx->ev[3], s);
