@@ -27,7 +27,10 @@ namespace qsg {
 namespace {  // internal linkage: every batch_layout_*.cu gets its own copy
 
 constexpr int kMaxB = 32;       // slots per batch (B = 8 CTA-local, 32 grid-wide)
-constexpr int kThreads = 512;   // 16 warps
+#ifndef QSG_BATCH_THREADS
+#define QSG_BATCH_THREADS 512
+#endif
+constexpr int kThreads = QSG_BATCH_THREADS;  // 16 warps by default
 constexpr int W = kThreads / 32;
 constexpr int NBUF = 12;
 #ifndef QSG_BATCH_UNROLL
@@ -999,27 +1002,44 @@ int cluster_capacity(int cs) {
 }  // namespace
 }  // namespace qsg
 
+namespace qsg {
+namespace {
+// Per-layout entry points as templates, so `if constexpr` discards the other group modes and each
+// translation unit instantiates exactly one kernel.
+template <int BS, int GM>
+int layout_occ() {
+  return occupancy_of<BS, GM>();
+}
+template <int BS, int GM>
+int layout_clusters(int cs) {
+  if constexpr (GM == GM_CLUSTER) return cluster_capacity<BS>(cs);
+  else return 0;
+}
+template <int BS, int GM>
+cudaError_t layout_launch(const BatchProblem& P, int grid, int cs, cudaStream_t s) {
+  if constexpr (GM == GM_CLUSTER) {
+    return launch_cluster<BS>(P, grid, cs, s);
+  } else if constexpr (GM == GM_GRID) {
+    void* args[] = {const_cast<BatchProblem*>(&P)};
+    set_attrs<BS, GM_GRID>();
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(batch_kernel<BS, GM_GRID>), dim3(grid),
+                                       dim3(kThreads), args, dyn_smem<BS, GM_GRID>(), s);
+  } else {
+    set_attrs<BS, GM_CTA>();
+    batch_kernel<BS, GM_CTA><<<grid, kThreads, dyn_smem<BS, GM_CTA>(), s>>>(P);
+    return cudaGetLastError();
+  }
+}
+}  // namespace
+}  // namespace qsg
+
 // Defines the per-layout entry points of one kernel instantiation (one translation unit each, so
 // the seven instantiations compile in parallel).
 #define QSG_BATCH_LAYOUT(ID, BS, GM)                                                              \
   namespace qsg {                                                                                 \
-  int batch_layout_occ_##ID() { return occupancy_of<BS, GM>(); }      \
-  int batch_layout_clusters_##ID(int cs) {                                                        \
-    if constexpr (GM == GM_CLUSTER) return cluster_capacity<BS>(cs); \
-    else return 0;                                                                                \
-  }                                                                                               \
+  int batch_layout_occ_##ID() { return layout_occ<BS, GM>(); }                                    \
+  int batch_layout_clusters_##ID(int cs) { return layout_clusters<BS, GM>(cs); }                  \
   cudaError_t batch_layout_launch_##ID(const BatchProblem& P, int grid, int cs, cudaStream_t s) { \
-    if constexpr (GM == GM_CLUSTER) {                                                             \
-      return launch_cluster<BS>(P, grid, cs, s);                                                  \
-    } else if constexpr (GM == GM_GRID) {                                                         \
-      void* args[] = {const_cast<BatchProblem*>(&P)};                                             \
-      set_attrs<BS, GM_GRID>();                                                                   \
-      return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(batch_kernel<BS, GM_GRID>), dim3(grid), \
-                                         dim3(kThreads), args, dyn_smem<BS, GM_GRID>(), s);       \
-    } else {                                                                                      \
-      set_attrs<BS, GM_CTA>();                                                                    \
-      batch_kernel<BS, GM_CTA><<<grid, kThreads, dyn_smem<BS, GM_CTA>(), s>>>(P);                 \
-      return cudaGetLastError();                                                                  \
-    }                                                                                             \
+    return layout_launch<BS, GM>(P, grid, cs, s);                                                 \
   }                                                                                               \
   }

@@ -114,8 +114,6 @@ __device__ __forceinline__ double2 sell_row_at(const DevSell& A, int row, XF&& x
   return acc;
 }
 
-__device__ __forceinline__ double2 rscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
-
 // T threads per trajectory: one warp for small systems (many trajectories per SM, cheap barriers),
 // 256 for large ones.
 template <int MODE, int T>
