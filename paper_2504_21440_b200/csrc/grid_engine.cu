@@ -182,7 +182,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-template <int S, bool PF>
+// X2 (stage 2 only): the stage input y + h a21 k1 was materialised in SB by x2_pass, so the SpMV
+// gathers one vector instead of two.
+template <int S, bool PF, bool X2 = false>
 __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c, int s0, int s1,
                                              const double2* sval = nullptr, const int* soff = nullptr) {
   using namespace dp;
@@ -200,7 +202,8 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
   };
   const double2* __restrict__ y = gptr(c.p[Y]);
   const double2* __restrict__ k1 = gptr(c.p[K1]);
-  const double2* __restrict__ x = S == 2 ? nullptr : gptr((S == 3 || S == 5 || S == 7) ? c.p[SA] : c.p[SB]);
+  const double2* __restrict__ x = S == 2 ? (X2 ? gptr(c.p[SB]) : nullptr)
+                                         : gptr((S == 3 || S == 5 || S == 7) ? c.p[SA] : c.p[SB]);
   const double2* __restrict__ pk2 = gptr(c.p[K2]);
   const double2* __restrict__ pk3 = gptr(c.p[K3]);
   const double2* __restrict__ pk4 = gptr(c.p[K4]);
@@ -226,7 +229,7 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
     o.y1 = (S == 7 && ok) ? ldo(x + row) : z;
   };
   auto xin = [&](int col) {
-    if constexpr (S == 2) {
+    if constexpr (S == 2 && !X2) {
       const double2 a = y[col], q = k1[col];
       return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
     } else {
@@ -332,6 +335,20 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
     epilogue(row, k, o);
   }
   return esq;
+}
+
+// SB = y + h a21 k1 over this CTA's rows: the stage-2 input, same expression as the on-the-fly
+// gather (integrator.hpp:91), so the result is bit-identical
+__device__ __noinline__ void x2_pass(const GridProblem& P, const Ctl& c, int s0, int s1) {
+  const double2* __restrict__ y = c.p[Y];
+  const double2* __restrict__ k1 = c.p[K1];
+  double2* __restrict__ sb = c.p[SB];
+  const double hh = c.hh;
+  const int r0 = s0 * 32, r1 = min(P.n, s1 * 32);
+  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const double2 a = ld_na_c2(y + r), q = ld_na_c2(k1 + r);
+    sb[r] = make_double2(a.x + hh * (dp::a21 * q.x), a.y + hh * (dp::a21 * q.y));
+  }
 }
 
 // start (integrator.hpp:61-69): k1 = G(t0) y and the d0/d1 norms of initial_step (:160-167)
@@ -558,7 +575,13 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     __syncthreads();
     if (c.done || c.status != kRunning) break;
     // stage 2 (+ observations of the previous accepted step)
-    stage_pass<2, PF>(P, c, s0, s1, sval, soff);
+    if (PF && P.x2) {
+      x2_pass(P, c, s0, s1);
+      grid_barrier(P.bar, G);
+      stage_pass<2, PF, true>(P, c, s0, s1, sval, soff);
+    } else {
+      stage_pass<2, PF>(P, c, s0, s1, sval, soff);
+    }
     if (c.np) observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
     grid_barrier(P.bar, G);
     if (c.np) {

@@ -21,6 +21,7 @@ struct GridCtl {
 
 struct GridProblem {
   int smem_dict;  // > 0: the single-term coded generator's dictionary (entries) staged in shared memory
+  int x2;         // materialise the stage-2 input (one extra pass + barrier, half the stage-2 gathers)
   int n;     // vector length (d*d for mesolve, d for sesolve)
   int d;     // Hilbert dimension
   DevGen gen;
