@@ -214,9 +214,15 @@ __global__ void sell_fill_kernel(const int* rowptr, const int* col, const double
 }
 
 // ---- dictionary of distinct (column - row, value) pairs, built on the device -------------------
-// Lock-free open addressing: a 64-bit signature claims a slot by CAS, the owner then publishes the
-// full key; equal signatures are confirmed against the full key (exact bit patterns), so the
-// dictionary is lossless. Dense ids follow slot order, which depends only on the keys.
+// Lock-free open addressing in two launches, with no thread ever waiting on another:
+//  claim:  each entry's 64-bit signature claims an empty slot by CAS (or finds it already there);
+//          the claiming thread writes the full key into its slot;
+//  lookup: after the claim launch has completed, every entry probes again and must find its FULL
+//          key (exact bit patterns) under its signature. Two distinct keys sharing a signature
+//          leave one of them unfound, which sets `overflow` and keeps the operator plain, so the
+//          dictionary is lossless by construction.
+// The set of keys is fixed by the operator; which slot (and so which code) a key gets can depend
+// on claim order, the decoded operator cannot.
 constexpr unsigned kDictSlots = 1u << 17;
 
 __device__ __forceinline__ unsigned long long pair_sig(int off, unsigned long long re, unsigned long long im) {
@@ -228,8 +234,37 @@ __device__ __forceinline__ unsigned long long pair_sig(int off, unsigned long lo
   return h | 1ull;
 }
 
-__global__ void dict_insert_kernel(const int* rowptr, const int* col, const double2* val, int n,
-                                   unsigned long long* tsig, int* toff, double2* tval, int* ready,
+__global__ void dict_claim_kernel(const int* rowptr, const int* col, const double2* val, int n,
+                                  unsigned long long* tsig, int* toff, double2* tval, int* overflow) {
+  const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int p = rowptr[r]; p < rowptr[r + 1]; ++p) {
+    const int off = col[p] - static_cast<int>(r);
+    const double2 v = val[p];
+    const unsigned long long sg =
+        pair_sig(off, __double_as_longlong(v.x), __double_as_longlong(v.y));
+    unsigned slot = static_cast<unsigned>(sg >> 20) & (kDictSlots - 1);
+    bool done = false;
+    for (unsigned probe = 0; probe < kDictSlots && !done; ++probe) {
+      // read first: with few distinct pairs almost every entry finds its signature in place and
+      // needs no atomic; only an empty slot is claimed with CAS (a stale 0 just falls through to it)
+      unsigned long long prev = *reinterpret_cast<volatile unsigned long long*>(tsig + slot);
+      if (prev == 0ull) {
+        prev = atomicCAS(tsig + slot, 0ull, sg);
+        if (prev == 0ull) {
+          toff[slot] = off;
+          tval[slot] = v;
+        }
+      }
+      done = prev == 0ull || prev == sg;
+      slot = (slot + 1) & (kDictSlots - 1);
+    }
+    if (!done) atomicExch(overflow, 1);
+  }
+}
+
+__global__ void dict_lookup_kernel(const int* rowptr, const int* col, const double2* val, int n,
+                                   const unsigned long long* tsig, const int* toff, const double2* tval,
                                    unsigned* slot_of, int* overflow) {
   const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n) return;
@@ -239,31 +274,22 @@ __global__ void dict_insert_kernel(const int* rowptr, const int* col, const doub
     const unsigned long long re = __double_as_longlong(v.x), im = __double_as_longlong(v.y);
     const unsigned long long sg = pair_sig(off, re, im);
     unsigned slot = static_cast<unsigned>(sg >> 20) & (kDictSlots - 1);
-    bool placed = false;
-    for (unsigned probe = 0; probe < kDictSlots && !placed; ++probe) {
-      const unsigned long long prev = atomicCAS(tsig + slot, 0ull, sg);
-      if (prev == 0ull) {
-        toff[slot] = off;
-        tval[slot] = v;
-        __threadfence();
-        atomicExch(ready + slot, 1);
-        slot_of[p] = slot;
-        placed = true;
-      } else if (prev == sg) {
-        while (atomicAdd(ready + slot, 0) == 0) {
-        }
-        __threadfence();
-        const volatile int* vo = toff + slot;
-        const volatile double* vv = reinterpret_cast<const volatile double*>(tval + slot);
-        if (*vo == off && __double_as_longlong(vv[0]) == static_cast<long long>(re) &&
-            __double_as_longlong(vv[1]) == static_cast<long long>(im)) {
+    bool found = false;
+    for (unsigned probe = 0; probe < kDictSlots; ++probe) {
+      const unsigned long long t = tsig[slot];
+      if (t == 0ull) break;
+      if (t == sg) {
+        const double2 kv = tval[slot];
+        if (toff[slot] == off && static_cast<unsigned long long>(__double_as_longlong(kv.x)) == re &&
+            static_cast<unsigned long long>(__double_as_longlong(kv.y)) == im) {
           slot_of[p] = slot;
-          placed = true;
+          found = true;
+          break;
         }
       }
       slot = (slot + 1) & (kDictSlots - 1);
     }
-    if (!placed) atomicExch(overflow, 1);
+    if (!found) atomicExch(overflow, 1);
   }
 }
 
@@ -315,20 +341,20 @@ static cudaError_t build_coded_store(qsg_op* op, const int* rp, const int* col, 
                                      const std::vector<long long>& w, cudaStream_t s) {
   const long long nsl = static_cast<long long>(w.size());
   cudaError_t e;
-  DevBuf tsig, toff, tval, ready, slot_of, dense, cnt, ovf, doff, dval;
+  DevBuf tsig, toff, tval, slot_of, dense, cnt, ovf, doff, dval;
   if ((e = tsig.alloc(sizeof(unsigned long long) * kDictSlots, s)) || (e = toff.alloc(sizeof(int) * kDictSlots, s)) ||
-      (e = tval.alloc(sizeof(double2) * kDictSlots, s)) || (e = ready.alloc(sizeof(int) * kDictSlots, s)) ||
+      (e = tval.alloc(sizeof(double2) * kDictSlots, s)) ||
       (e = slot_of.alloc(sizeof(unsigned) * op->nnz, s)) || (e = dense.alloc(sizeof(unsigned) * kDictSlots, s)) ||
       (e = cnt.alloc(sizeof(int), s)) || (e = ovf.alloc(sizeof(int), s)) ||
       (e = doff.alloc(sizeof(int) * 65536, s)) || (e = dval.alloc(sizeof(double2) * 65536, s)))
     return e;
   cudaMemsetAsync(tsig.p, 0, sizeof(unsigned long long) * kDictSlots, s);
-  cudaMemsetAsync(ready.p, 0, sizeof(int) * kDictSlots, s);
   cudaMemsetAsync(ovf.p, 0, sizeof(int), s);
   const unsigned nb = static_cast<unsigned>((n + 255) / 256);
-  dict_insert_kernel<<<nb, 256, 0, s>>>(rp, col, val, static_cast<int>(n), tsig.as<unsigned long long>(),
-                                        toff.as<int>(), tval.as<double2>(), ready.as<int>(), slot_of.as<unsigned>(),
-                                        ovf.as<int>());
+  dict_claim_kernel<<<nb, 256, 0, s>>>(rp, col, val, static_cast<int>(n), tsig.as<unsigned long long>(),
+                                       toff.as<int>(), tval.as<double2>(), ovf.as<int>());
+  dict_lookup_kernel<<<nb, 256, 0, s>>>(rp, col, val, static_cast<int>(n), tsig.as<unsigned long long>(),
+                                        toff.as<int>(), tval.as<double2>(), slot_of.as<unsigned>(), ovf.as<int>());
   dict_compact_kernel<<<1, 1024, 0, s>>>(tsig.as<unsigned long long>(), toff.as<int>(), tval.as<double2>(),
                                          dense.as<unsigned>(), doff.as<int>(), dval.as<double2>(), 65536,
                                          cnt.as<int>());
