@@ -90,6 +90,25 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
                                : 4;
   }
   int cs = 16;
+  // mesolve parameter sweeps (configs[4]): one point per cluster of cs CTAs, cs the smallest size
+  // whose co-resident points' state fits 1.5x L2 while every CTA slot still has work (16 when
+  // there are too few points to fill the GPU otherwise, e.g. a sharded sweep). Coupled Kerr
+  // 10x10, 256 points (scripts/probe_sweep.py): 158 ms one point per CTA; clusters of 2/4/8/16
+  // CTAs 117/102/118/178 ms (4 CTAs: 74 points x 2.2 MB in flight). mcsolve keeps one trajectory
+  // per CTA: its jump and norm bookkeeping made the cluster layouts no faster (section above).
+  if (layout == 4 && P.mode == 1 && P.n >= 4096 && !std::getenv("QSG_BATCH_MODE")) {
+    const double state = static_cast<double>(batch_work_stride(P.n, 5)) * sizeof(double2);
+    for (int c = 2; c <= 16; c *= 2) {
+      const int cap = batch_max_clusters(5, c);
+      if (cap <= 0) break;
+      if (n_sys * c < slots1 && c < 16) continue;  // few points: wider clusters keep the SMs busy
+      if (std::min<long long>(cap, n_sys) * state <= 1.5 * static_cast<double>(ctx->l2_bytes)) {
+        layout = 5;
+        cs = c;
+        break;
+      }
+    }
+  }
   if (const char* c = std::getenv("QSG_CLUSTER")) cs = std::max(1, std::min(16, std::atoi(c)));
   const bool grid_mode = layout == 1;
   const bool cluster_mode = layout == 5 || layout == 6;
