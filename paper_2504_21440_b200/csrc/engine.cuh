@@ -354,11 +354,16 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// bar[0] = arrival count, bar[1] = generation. All CTAs of the grid participate.
+// All CTAs of the grid participate. `bar` holds 8 bytes, 8-byte aligned, zeroed before the launch.
 #ifdef QSG_BAR_TIMING  // development build: total ns CTAs spend waiting in grid barriers
 static __device__ unsigned long long g_bar_wait_ns, g_bar_calls, g_bar_cta_ns[1024];
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -373,6 +378,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int G) {
 #ifdef QSG_BAR_TIMING
   const unsigned long long t_in = threadIdx.x == 0 ? gtimer() : 0ull;
 #endif
+#ifdef QSG_BAR_V1
   if (G > 1 && threadIdx.x == 0) {
     const unsigned gen = ld_acquire_gpu(bar + 1);
     __threadfence();
@@ -387,6 +393,20 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int G) {
     }
     __threadfence();
   }
+#else
+  // One monotone 64-bit arrival counter (bar[0..1], zeroed before the launch): barrier k is open
+  // once the counter reaches (k+1)*G. A CTA's own arrival returns a value in [k*G, (k+1)*G), which
+  // names k, so no generation word, reset or release store is needed: the last arrival's atomic is
+  // the only write between the arrivals and the waiters' next poll.
+  if (G > 1 && threadIdx.x == 0) {
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(bar);
+    __threadfence();
+    const unsigned long long old = atomicAdd(cnt, 1ull);
+    const unsigned long long target = (old / static_cast<unsigned long long>(G) + 1) * static_cast<unsigned long long>(G);
+    while (ld_acquire_gpu_u64(cnt) < target) {
+    }
+  }
+#endif
 #ifdef QSG_BAR_TIMING
   if (threadIdx.x == 0) {
     const unsigned long long dt = gtimer() - t_in;
