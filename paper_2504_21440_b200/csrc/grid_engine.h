@@ -49,7 +49,8 @@ struct GridProblem {
   double2* states;  // n_save x n
   GridCtl* ctl;
   double* red;       // kNumSlots x G partials
-  unsigned* bar;     // grid barrier {count, generation}
+  unsigned* bar;     // grid barrier: one 64-bit arrival counter
+  const int* part;   // G+1 slice boundaries per CTA (null: even split)
 };
 
 int grid_threads();
