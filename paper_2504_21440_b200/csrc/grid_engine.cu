@@ -467,8 +467,7 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
   const int G = gridDim.x, rank = blockIdx.x;
   const int nsl = (P.n + 31) >> 5;
   const int spc = (nsl + G - 1) / G;
-  const int s0 = P.part ? P.part[rank] : rank * spc;
-  const int s1 = P.part ? P.part[rank + 1] : min(nsl, rank * spc + spc);
+  const int s0 = rank * spc, s1 = min(nsl, s0 + spc);
   double* red = P.red;
   const int kcap = max(1, min(kMaxPending, kObsSlots / (2 * max(1, P.n_e))));
   auto slots = [&](int par) { return red + static_cast<long long>(kSlotObs0 + par * kObsSlots) * G; };

@@ -50,7 +50,6 @@ struct GridProblem {
   GridCtl* ctl;
   double* red;       // kNumSlots x G partials
   unsigned* bar;     // grid barrier: one 64-bit arrival counter
-  const int* part;   // G+1 slice boundaries per CTA (null: even split)
 };
 
 int grid_threads();

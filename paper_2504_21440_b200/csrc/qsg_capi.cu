@@ -543,7 +543,7 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
     P.se_off = d_soff.as<long long>();
   }
   // ---- outputs and control
-  DevBuf d_exp, d_states, d_ctl, d_red, d_bar, d_part;
+  DevBuf d_exp, d_states, d_ctl, d_red, d_bar;
   if ((ce = d_exp.alloc(std::max<size_t>(1, static_cast<size_t>(n_e) * n_t) * sizeof(double2), s)))
     return cuda_fail(ce, "expect");
   cudaMemsetAsync(d_exp.p, 0, std::max<size_t>(1, static_cast<size_t>(n_e) * n_t) * sizeof(double2), s);
@@ -589,34 +589,6 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   P.ctl = d_ctl.as<GridCtl>();
   P.red = d_red.as<double>();
   P.bar = d_bar.as<unsigned>();
-  // Slices per CTA by cost (entries per row + alpha per row for the vector work), summed over the
-  // generator's terms, instead of an even count: QSG_PART_ALPHA=<alpha> (negative: even split).
-  P.part = nullptr;
-  double alpha = -1.0;
-  if (const char* pa = std::getenv("QSG_PART_ALPHA")) alpha = std::atof(pa);
-  const long long nsl = (n + 31) / 32;
-  bool have_w = alpha >= 0.0 && grid > 1;
-  for (int k = 0; k < G->n_terms && have_w; ++k) have_w = static_cast<long long>(G->ops[k]->slice_w.size()) == nsl;
-  if (have_w) {
-    std::vector<double> pre(nsl + 1, 0.0);
-    for (long long i = 0; i < nsl; ++i) {
-      double c = alpha;
-      for (int k = 0; k < G->n_terms; ++k) c += G->ops[k]->slice_w[i];
-      pre[i + 1] = pre[i] + c;
-    }
-    std::vector<int> part(grid + 1, 0);
-    long long b = 0;
-    for (int r = 1; r < grid; ++r) {
-      const double tgt = pre[nsl] * r / grid;
-      while (b < nsl && pre[b + 1] <= tgt) ++b;
-      if (b < nsl && tgt - pre[b] > pre[b + 1] - tgt) ++b;  // nearest boundary
-      part[r] = static_cast<int>(std::max<long long>(b, part[r - 1]));
-    }
-    part[grid] = static_cast<int>(nsl);
-    if ((ce = d_part.alloc(sizeof(int) * (grid + 1), s))) return cuda_fail(ce, "partition");
-    cudaMemcpyAsync(d_part.p, part.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice, s);
-    P.part = d_part.as<int>();
-  }
   cudaEventRecord(ctx->ev[0], s);
   if ((ce = launch_grid_dp5(P, mode, pf, grid, s))) return cuda_fail(ce, "solver launch");
   cudaEventRecord(ctx->ev[1], s);
@@ -774,7 +746,6 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
     op->max_rowlen = std::max<int>(op->max_rowlen, static_cast<int>(w[i]));
   }
   op->padded_cols = off[nsl];
-  op->slice_w.assign(w.begin(), w.end());
   const size_t pe = static_cast<size_t>(std::max<long long>(1, off[nsl] * 32));
   if ((e = cudaMallocAsync(&op->col, sizeof(int) * pe, s)) || (e = cudaMallocAsync(&op->val, sizeof(double2) * pe, s))) {
     qsg_op_destroy(op);

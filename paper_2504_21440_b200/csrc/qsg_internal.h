@@ -35,7 +35,6 @@ struct qsg_op {
   int* col = nullptr;
   double2* val = nullptr;
   int max_rowlen = 0;
-  std::vector<int> slice_w;  // host copy of the per-slice widths (grid-engine partition)
   // dictionary-coded entries (engine.cuh DevSell): 0 = plain, 1 = uint8, 2 = uint16 codes
   int code_bytes = 0;
   long long* code_off = nullptr;  // per slice, in entries (row-contiguous code blocks)
