@@ -36,6 +36,9 @@ struct DevSell {
   const int* dict_off;
   const double2* dict_val;
   int dict_n;  // dictionary entries (0 when plain)
+  // plain store small enough that each SM's share of it stays in L1 across passes: its (col, val)
+  // entries are loaded through the L1-allocating read-only path instead of L1::no_allocate
+  int l1;
 };
 
 struct DevCoeff {
@@ -277,34 +280,37 @@ __device__ __forceinline__ double2 sell_row_coded(const DevSell& A, int row, int
   return acc;
 }
 
+// plain-store row: L1 = entries through the L1-allocating read-only path (DevSell::l1)
+template <bool L1, class XF>
+__device__ __forceinline__ double2 sell_row_plain(const DevSell& A, int len, long long base, XF&& xf) {
+  double2 acc = make_double2(0.0, 0.0);
+  for (int j = 0; j < len; j += 8) {
+    int c[8];
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (j + u < len) {
+        c[u] = L1 ? __ldg(A.col + base + 32LL * (j + u)) : ld_stream(A.col + base + 32LL * (j + u));
+        v[u] = L1 ? __ldg(A.val + base + 32LL * (j + u)) : ld_stream(A.val + base + 32LL * (j + u));
+      } else {
+        c[u] = 0;
+        v[u] = make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j + u < len) cfma(v[u], xf(c[u]), acc);
+  }
+  return acc;
+}
+
 template <class XF>
 __device__ __forceinline__ double2 sell_row(const DevSell& A, int slice, int lane, XF&& xf) {
   const int len = __ldg(A.rowlen + slice * 32 + lane);
   const long long base = __ldg(A.slice_off + slice) * 32 + lane;
   const int row = slice * 32 + lane;
-  double2 acc = make_double2(0.0, 0.0);
-  if (A.code_bytes == 0) {
-    for (int j = 0; j < len; j += 8) {
-      int c[8];
-      double2 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (j + u < len) {
-          c[u] = ld_stream(A.col + base + 32LL * (j + u));
-          v[u] = ld_stream(A.val + base + 32LL * (j + u));
-        } else {
-          c[u] = 0;
-          v[u] = make_double2(0.0, 0.0);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (j + u < len) cfma(v[u], xf(c[u]), acc);
-    }
-  } else {
-    acc = sell_row_coded(A, row, len, __ldg(A.code_off + slice) + 8LL * lane, xf);
-  }
-  return acc;
+  if (A.code_bytes != 0) return sell_row_coded(A, row, len, __ldg(A.code_off + slice) + 8LL * lane, xf);
+  return A.l1 ? sell_row_plain<true>(A, len, base, xf) : sell_row_plain<false>(A, len, base, xf);
 }
 
 // Row `slice*32 + lane` of G(t) x with the reference term order: out = A0 x; out += c_k (A_k x)

@@ -55,6 +55,12 @@ DevSell sell_view(const qsg_op* op, bool use_codes) {
   v.dict_off = op->dict_off;
   v.dict_val = op->dict_val;
   v.dict_n = op->dict_n;
+  // L1-cached plain entries while the whole plain store is at most QSG_L1OP_MAX_BYTES (default
+  // 64 MB; Kerr N=400, 19 MB: 316 -> 251 ms per solve; the 493 MB TFIM-10 plain store streams
+  // from HBM and is faster with L1::no_allocate, 55.3 vs 61.4 ms, profiles/r01_l1op_ab.log)
+  const char* l1e = std::getenv("QSG_L1OP_MAX_BYTES");
+  const long long l1_max = l1e ? std::atoll(l1e) : (64LL << 20);
+  v.l1 = v.code_bytes == 0 && 20 * op->nnz <= l1_max;
   return v;
 }
 
