@@ -137,26 +137,34 @@ __device__ double rng_uniform_pos(unsigned long long* s) {
 
 // Logical buffer k of slot s lives in physical array map[s][k]: an accepted step relabels
 // (Y, YO, Y1) and (K1, K1O, K7) instead of copying them (FSAL, integrator.hpp:135-137).
-template <int BS>
+template <int BS, bool NA = true>
 struct Ctx {
   const BatchProblem& P;
   double2* w;  // batch workspace: NBUF arrays of [n][BS]
   int n;
   const unsigned char (*map)[NBUF];  // shared memory, per slot
   __device__ double2* buf(int k, int s) const { return w + static_cast<long long>(map[s][k]) * n * BS; }
-  __device__ double2 ld(int k, int r, int s) const { return buf(k, s)[static_cast<long long>(r) * BS + s]; }
+  // ld: operands streamed once per pass (NA: L1::no_allocate keeps L1 for the gathers; measured
+  // +1.8% on TFIM-14 mcsolve, -2.4% on the cluster-layout sweep, so cluster layouts keep L1
+  // allocation); ldx: gathers and dense-output reads (L1-allocating)
+  __device__ double2 ld(int k, int r, int s) const {
+    const double2* p = buf(k, s) + static_cast<long long>(r) * BS + s;
+    if constexpr (NA) return ld_na_c2(p);
+    else return *p;
+  }
+  __device__ double2 ldx(int k, int r, int s) const { return buf(k, s)[static_cast<long long>(r) * BS + s]; }
   __device__ void st(int k, int r, int s, double2 v) const { buf(k, s)[static_cast<long long>(r) * BS + s] = v; }
 };
 
 // dense output of slot s at index c (integrator.hpp:127-131,150-154) from the committed step
-template <int BS>
-__device__ __forceinline__ double2 dense_at(const Ctx<BS>& C, int c, int s, double theta, double h, int src) {
-  if (src == SRC_Y) return C.ld(Y, c, s);
-  if (src == SRC_SC) return C.ld(SC, c, s);
+template <int BS, bool NA>
+__device__ __forceinline__ double2 dense_at(const Ctx<BS, NA>& C, int c, int s, double theta, double h, int src) {
+  if (src == SRC_Y) return C.ldx(Y, c, s);
+  if (src == SRC_SC) return C.ldx(SC, c, s);
   using namespace dp;
   // after the commit relabelling K1 holds the step's k7 (FSAL) and K1O its k1
-  const double2 yo = C.ld(YO, c, s), y1 = C.ld(Y, c, s), k1 = C.ld(K1O, c, s), k7 = C.ld(K1, c, s);
-  const double2 k3 = C.ld(K3, c, s), k4 = C.ld(K4, c, s), k5 = C.ld(K5, c, s), k6 = C.ld(K6, c, s);
+  const double2 yo = C.ldx(YO, c, s), y1 = C.ldx(Y, c, s), k1 = C.ldx(K1O, c, s), k7 = C.ldx(K1, c, s);
+  const double2 k3 = C.ldx(K3, c, s), k4 = C.ldx(K4, c, s), k5 = C.ldx(K5, c, s), k6 = C.ldx(K6, c, s);
   const double th1 = 1.0 - theta;
   const double2 rc2 = csub(y1, yo);
   const double2 rc3 = csub(cscale(h, k1), rc2);
@@ -353,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
   const int g_rank = GRID ? static_cast<int>(blockIdx.x) : CLU ? static_cast<int>(cluster_rank()) : 0;
   const int g_size = GRID ? static_cast<int>(gridDim.x) : CLU ? static_cast<int>(cluster_size()) : 1;
   const long long batch_id = GRID ? 0LL : CLU ? static_cast<long long>(blockIdx.x) / g_size : blockIdx.x;
-  const Ctx<BS> C{P, P.work + batch_id * P.work_stride, n, s_map};
+  const Ctx<BS, !CLU> C{P, P.work + batch_id * P.work_stride, n, s_map};
   const double atol = P.atol, rtol = P.rtol, eps_t = P.eps_t, tf = P.tf, t0 = P.t0;
   const bool out_cta = g_rank == 0;  // the CTA of a group that writes per-system outputs
   const int rpc = PART ? (n + g_size - 1) / g_size : n;
@@ -493,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       const double* prm = slot_params(P, S[sl]);
       if (ph == START) {
         rows([&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, t0, [&](int c) { return C.ld(Y, c, sl); });
+          const double2 k = gen_row_slot(P.gen, prm, r, t0, [&](int c) { return C.ldx(Y, c, sl); });
           C.st(K1, r, sl, k);
           const double2 yy = C.ld(Y, r, sl);
           const double sc = atol + rtol * cabs_(yy);
@@ -505,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         using namespace dp;
         rows_pf((1u << Y) | (1u << K1), [&](int r) {
           const double2 k = gen_row_slot(P.gen, prm, r, t + c2 * hh, [&](int c) {
-            const double2 a = C.ld(Y, c, sl), q = C.ld(K1, c, sl);
+            const double2 a = C.ldx(Y, c, sl), q = C.ldx(K1, c, sl);
             return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
           });
           const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl);
@@ -652,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         const double h0 = S[sl].h0;
         rows([&](int r) {
           const double2 k = gen_row_slot(P.gen, prm, r, t0 + h0, [&](int c) {
-            const double2 a = C.ld(Y, c, sl), q = C.ld(K1, c, sl);
+            const double2 a = C.ldx(Y, c, sl), q = C.ldx(K1, c, sl);
             return make_double2(a.x + h0 * q.x, a.y + h0 * q.y);
           });
           const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl);
@@ -664,7 +672,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
         rows_pf((1u << Y) | (1u << K1) | (1u << K2), [&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, t + c3 * hh, [&](int c) { return C.ld(SA, c, sl); });
+          const double2 k = gen_row_slot(P.gen, prm, r, t + c3 * hh, [&](int c) { return C.ldx(SA, c, sl); });
           const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl);
           C.st(K3, r, sl, k);
           C.st(SB, r, sl, make_double2(yy.x + hh * (a41 * q1.x + a42 * q2.x + a43 * k.x),
@@ -704,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
         rows_pf((1u << Y) | (1u << K1) | (1u << K2) | (1u << K3), [&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, t + c4 * hh, [&](int c) { return C.ld(SB, c, sl); });
+          const double2 k = gen_row_slot(P.gen, prm, r, t + c4 * hh, [&](int c) { return C.ldx(SB, c, sl); });
           const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl), q3 = C.ld(K3, r, sl);
           C.st(K4, r, sl, k);
           C.st(SA, r, sl, make_double2(yy.x + hh * (a51 * q1.x + a52 * q2.x + a53 * q3.x + a54 * k.x),
@@ -714,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         // restart: integ.start(jump_t, psi, tf, h_current) (trajectories.cpp:202-203)
         const double tj = S[sl].jump_t;
         rows([&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, tj, [&](int c) { return C.ld(SC, c, sl); });
+          const double2 k = gen_row_slot(P.gen, prm, r, tj, [&](int c) { return C.ldx(SC, c, sl); });
           C.st(K1, r, sl, k);
           C.st(Y, r, sl, C.ld(SC, r, sl));
         });
@@ -745,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       const double hh = S[sl].hh, t = S[sl].t;
       using namespace dp;
       rows_pf((1u << Y) | (1u << K1) | (1u << K2) | (1u << K3) | (1u << K4), [&](int r) {
-        const double2 k = gen_row_slot(P.gen, prm, r, t + c5 * hh, [&](int c) { return C.ld(SA, c, sl); });
+        const double2 k = gen_row_slot(P.gen, prm, r, t + c5 * hh, [&](int c) { return C.ldx(SA, c, sl); });
         const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl), q3 = C.ld(K3, r, sl),
                       q4 = C.ld(K4, r, sl);
         C.st(K5, r, sl, k);
@@ -760,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       const double hh = S[sl].hh, t = S[sl].t;
       using namespace dp;
       rows_pf((1u << Y) | (1u << K1) | (1u << K3) | (1u << K4) | (1u << K5), [&](int r) {
-        const double2 k = gen_row_slot(P.gen, prm, r, t + hh, [&](int c) { return C.ld(SB, c, sl); });
+        const double2 k = gen_row_slot(P.gen, prm, r, t + hh, [&](int c) { return C.ldx(SB, c, sl); });
         const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q3 = C.ld(K3, r, sl), q4 = C.ld(K4, r, sl),
                       q5 = C.ld(K5, r, sl);
         C.st(K6, r, sl, k);
@@ -779,7 +787,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
         rows_pf((1u << Y) | (1u << Y1) | (1u << K1) | (1u << K3) | (1u << K4) | (1u << K5) | (1u << K6), [&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, t + hh, [&](int c) { return C.ld(Y1, c, sl); });
+          const double2 k = gen_row_slot(P.gen, prm, r, t + hh, [&](int c) { return C.ldx(Y1, c, sl); });
           const double2 yy = C.ld(Y, r, sl), y1 = C.ld(Y1, r, sl), q1 = C.ld(K1, r, sl), q3 = C.ld(K3, r, sl),
                         q4 = C.ld(K4, r, sl), q5 = C.ld(K5, r, sl), q6 = C.ld(K6, r, sl);
           C.st(K7, r, sl, k);
