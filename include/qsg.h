@@ -107,6 +107,8 @@ typedef struct {
   int64_t attempts;   /* DP5 attempts (accepted + rejected) executed on device */
   int32_t grid_ctas;  /* CTAs cooperating on one system */
   int32_t lanes;      /* lanes per CSR row in the SpMV */
+  int32_t store;      /* operator store the solver streamed: 0 plain, 1 coded, 2 key-aligned */
+  int32_t reserved;
 } qsg_timing;
 
 /* ---- context / operator store ------------------------------------------------------- */
@@ -129,6 +131,13 @@ int64_t qsg_op_rows(const qsg_op* op);
  * Set QSG_NO_COMPRESS=1 to force the plain store. */
 int32_t qsg_op_code_bytes(const qsg_op* op);
 int32_t qsg_op_dict_size(const qsg_op* op);
+/* The stores an operator carries and the bytes one SpMV reads from each.
+ * info[0] = store the grid engine streams (0 plain, 1/2 coded, 3 key-aligned); info[1] plain
+ * bytes; info[2] coded bytes (0 if absent); info[3] key-aligned bytes (0 if absent); info[4]
+ * key-aligned distinct values; info[5] key-aligned positions; info[6] coded pairs; info[7]
+ * largest key-aligned slice block (bytes). The key-aligned store is built next to the coded one
+ * when it pays; QSG_NO_KA=1 disables it. */
+qsg_status qsg_op_store_info(const qsg_op* op, int64_t* info);
 
 /* On-device Liouvillian assembly (superop.cpp:78-91 liouvillian, :51-76 spre/spost/sprepost/
  * lindblad_dissipator): L = -i(I(x)H - H^T(x)I) + sum_k D(c_k) for d x d CSR operators H (may be

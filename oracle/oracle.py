@@ -59,6 +59,8 @@ def lib():
         L.orc_ising_capped.argtypes = [C.c_int, C.c_int]
         L.orc_model_prepare_liouvillian.argtypes = [P]
         L.orc_mesolve_prepared.argtypes = [P, DP, C.c_int, DP, C.c_int, DP, DP, LP]
+        L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_threads.restype = C.c_int
         _lib = L
     return _lib
 
@@ -249,6 +251,15 @@ class Model:
         _check(lib().orc_generator_apply(self._h, which, t, _dp(prm), len(prm),
                                          y.ctypes.data_as(DP), out.ctypes.data_as(DP)))
         return out
+
+
+def set_threads(n: int) -> None:
+    """Worker threads for single-solve loops; results are bit-identical to 1 thread."""
+    lib().orc_set_threads(int(n))
+
+
+def threads() -> int:
+    return int(lib().orc_threads())
 
 
 def rng(seed: int, stream: int, kind: int, n: int):

@@ -66,6 +66,10 @@ extern "C" {
 
 const char* orc_last_error(void) { return g_err.c_str(); }
 
+/// Worker threads for single-solve loops (bit-identical results; see qsim_oracle.hpp).
+void orc_set_threads(int n) { set_threads(n); }
+int orc_threads(void) { return threads(); }
+
 void* orc_model_new(const char* name, const double* p, int np) {
   try {
     auto h = std::make_unique<Handle>();

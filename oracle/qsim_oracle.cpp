@@ -5,10 +5,98 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <memory>
+#include <mutex>
 #include <numbers>
 #include <thread>
 
 namespace orc {
+
+// ---- worker pool (threads() > 1 only; see qsim_oracle.hpp) -------------------------------
+namespace {
+class Pool {
+ public:
+  explicit Pool(int n) : n_(n) {
+    for (int i = 1; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return n_; }
+  // f(tid) on every worker and the caller; returns when all are done
+  void run(const std::function<void(int)>& f) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      job_ = &f;
+      pending_ = n_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void loop(int tid) {
+    long seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        f = job_;
+      }
+      (*f)(tid);
+      std::lock_guard<std::mutex> g(m_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  int n_;
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int pending_ = 0;
+  long gen_ = 0;
+  bool stop_ = false;
+};
+int g_threads = 1;
+std::unique_ptr<Pool> g_pool;
+
+// f(lo, hi) over a static split of [0, n)
+template <class F>
+void par_for(size_t n, F&& f, size_t min_n = 4096) {
+  if (g_threads <= 1 || n < min_n) {
+    f(size_t{0}, n);
+    return;
+  }
+  const size_t T = static_cast<size_t>(g_pool->size());
+  const std::function<void(int)> job = [&](int tid) {
+    const size_t lo = n * static_cast<size_t>(tid) / T, hi = n * static_cast<size_t>(tid + 1) / T;
+    if (lo < hi) f(lo, hi);
+  };
+  g_pool->run(job);
+}
+}  // namespace
+
+void set_threads(int n) {
+  n = std::max(1, n);
+  if (n == g_threads) return;
+  g_pool.reset();
+  g_threads = n;
+  if (n > 1) g_pool = std::make_unique<Pool>(n);
+}
+int threads() { return g_threads; }
 
 const char* error_code_name(ErrorCode c) {  // qobj.cpp:24-40
   switch (c) {
@@ -490,26 +578,73 @@ TdOp liouvillian_td(const TdOp& h, std::span<const QObj> c_ops) {  // evolve.cpp
   return out;
 }
 
+// CSC -> row-major, columns ascending within each row (stable counting sort by row)
+static CsrRows csc_rows(const Csc& a) {
+  CsrRows r;
+  r.rows = a.rows;
+  r.ptr.assign(static_cast<size_t>(a.rows + 1), 0);
+  for (int i : a.inner) ++r.ptr[static_cast<size_t>(i) + 1];
+  for (long i = 0; i < a.rows; ++i) r.ptr[static_cast<size_t>(i + 1)] += r.ptr[static_cast<size_t>(i)];
+  r.col.resize(a.inner.size());
+  r.val.resize(a.val.size());
+  std::vector<long> pos(r.ptr.begin(), r.ptr.end() - 1);
+  for (long j = 0; j < a.cols; ++j)
+    for (int p = a.outer[static_cast<size_t>(j)]; p < a.outer[static_cast<size_t>(j + 1)]; ++p) {
+      const long q = pos[static_cast<size_t>(a.inner[static_cast<size_t>(p)])]++;
+      r.col[static_cast<size_t>(q)] = static_cast<int>(j);
+      r.val[static_cast<size_t>(q)] = a.val[static_cast<size_t>(p)];
+    }
+  return r;
+}
+
+// Same per-row arithmetic as sp_gemv: out[i] = 0, then out[i] += v * (1 * y[j]) over the row's
+// entries in ascending column order (the order the CSC scatter reaches row i).
+static void rows_gemv(const CsrRows& a, const cd* y, cd* out) {
+  par_for(static_cast<size_t>(a.rows), [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi; ++i) {
+      cd acc(0.0, 0.0);
+      for (long p = a.ptr[i]; p < a.ptr[i + 1]; ++p) {
+        const cd rj = cd(1.0, 0.0) * y[a.col[static_cast<size_t>(p)]];
+        acc += a.val[static_cast<size_t>(p)] * rj;
+      }
+      out[i] = acc;
+    }
+  });
+}
+
 SparseGenerator::SparseGenerator(const TdOp& op, cd pref, const Params& params)
     : params_(params) {  // evolve.cpp:53-61
   const_part_ = (pref * op.constant).sparse();
   for (const auto& t : op.terms) terms_.emplace_back((pref * t.op).sparse(), t.coeff);
   tmp_.resize(static_cast<size_t>(const_part_.rows));
+  if (threads() > 1) {
+    const_rows_ = csc_rows(const_part_);
+    for (const auto& t : terms_) term_rows_.push_back(csc_rows(t.first));
+  }
 }
 
 void SparseGenerator::apply(double t, const std::vector<cd>& y, std::vector<cd>& out) const {
   // evolve.cpp:63-69
-  sp_gemv(const_part_, y.data(), out.data());
-  for (const auto& [mat, coeff] : terms_) {
-    sp_gemv(mat, y.data(), tmp_.data());
+  const bool rows = threads() > 1 && const_rows_.rows == const_part_.rows && const_rows_.rows > 0;
+  if (rows) rows_gemv(const_rows_, y.data(), out.data());
+  else sp_gemv(const_part_, y.data(), out.data());
+  for (size_t k = 0; k < terms_.size(); ++k) {
+    const auto& [mat, coeff] = terms_[k];
+    if (rows) rows_gemv(term_rows_[k], y.data(), tmp_.data());
+    else sp_gemv(mat, y.data(), tmp_.data());
     const cd c = coeff(params_, t);
-    for (size_t i = 0; i < out.size(); ++i) out[i] += c * tmp_[i];
+    par_for(out.size(), [&](size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; ++i) out[i] += c * tmp_[i];
+    });
   }
 }
 
 namespace {
 
 using Vec = std::vector<cd>;
+
+// element-wise loop body over i in [0, n), split over the worker pool when threads() > 1
+#define PAR(...) par_for(n, [&](size_t lo_, size_t hi_) { for (size_t i = lo_; i < hi_; ++i) { __VA_ARGS__; } })
 
 // integrator.hpp:23-195, every vector expression evaluated element-wise in Eigen order.
 template <class Rhs>
@@ -571,34 +706,32 @@ class Dopri5 {
       if (++attempts > 1000)
         throw_error(ErrorCode::IntegrationFailure,
                     "step repeatedly rejected at t = " + std::to_string(t_));
-      for (size_t i = 0; i < n; ++i) ysti_[i] = y_[i] + h * (a21 * k1_[i]);
+      PAR(ysti_[i] = y_[i] + h * (a21 * k1_[i]));
       rhs_(t_ + c2 * h, ysti_, k2_);
-      for (size_t i = 0; i < n; ++i) ysti_[i] = y_[i] + h * (a31 * k1_[i] + a32 * k2_[i]);
+      PAR(ysti_[i] = y_[i] + h * (a31 * k1_[i] + a32 * k2_[i]));
       rhs_(t_ + c3 * h, ysti_, k3_);
-      for (size_t i = 0; i < n; ++i)
-        ysti_[i] = y_[i] + h * (a41 * k1_[i] + a42 * k2_[i] + a43 * k3_[i]);
+      PAR(ysti_[i] = y_[i] + h * (a41 * k1_[i] + a42 * k2_[i] + a43 * k3_[i]));
       rhs_(t_ + c4 * h, ysti_, k4_);
-      for (size_t i = 0; i < n; ++i)
-        ysti_[i] = y_[i] + h * (a51 * k1_[i] + a52 * k2_[i] + a53 * k3_[i] + a54 * k4_[i]);
+      PAR(ysti_[i] = y_[i] + h * (a51 * k1_[i] + a52 * k2_[i] + a53 * k3_[i] + a54 * k4_[i]));
       rhs_(t_ + c5 * h, ysti_, k5_);
-      for (size_t i = 0; i < n; ++i)
-        ysti_[i] = y_[i] + h * (a61 * k1_[i] + a62 * k2_[i] + a63 * k3_[i] + a64 * k4_[i] +
-                                a65 * k5_[i]);
+      PAR(ysti_[i] = y_[i] + h * (a61 * k1_[i] + a62 * k2_[i] + a63 * k3_[i] + a64 * k4_[i] +
+                                  a65 * k5_[i]));
       rhs_(t_ + h, ysti_, k6_);
-      for (size_t i = 0; i < n; ++i)
-        ysti_[i] = y_[i] + h * (a71 * k1_[i] + a73 * k3_[i] + a74 * k4_[i] + a75 * k5_[i] +
-                                a76 * k6_[i]);
+      PAR(ysti_[i] = y_[i] + h * (a71 * k1_[i] + a73 * k3_[i] + a74 * k4_[i] + a75 * k5_[i] +
+                                  a76 * k6_[i]));
       rhs_(t_ + h, ysti_, k7_);
       rhs_evals_ += 6;
 
-      double err_sq = 0.0;  // :106-116
-      for (size_t i = 0; i < n; ++i) {
+      double err_sq = 0.0;  // :106-116 (terms element-wise, summed in index order)
+      q2_.resize(n);
+      PAR({
         const cd e = h * (e1 * k1_[i] + e3 * k3_[i] + e4 * k4_[i] + e5 * k5_[i] + e6 * k6_[i] +
                           e7 * k7_[i]);
         const double sc = atol_ + rtol_ * std::max(std::abs(y_[i]), std::abs(ysti_[i]));
         const double q = std::abs(e) / sc;
-        err_sq += q * q;
-      }
+        q2_[i] = q * q;
+      });
+      for (size_t i = 0; i < n; ++i) err_sq += q2_[i];
       double err = std::sqrt(err_sq / static_cast<double>(n));
       if (!std::isfinite(err)) err = 10.0;
 
@@ -608,19 +741,19 @@ class Dopri5 {
         fac = std::max(facc2, std::min(facc1, fac / safe));
         const double h_new = h / fac;
         facold_ = std::max(err, 1e-4);
-        for (size_t i = 0; i < n; ++i) {
+        PAR({
           rc1_[i] = y_[i];
           rc2_[i] = ysti_[i] - y_[i];
           rc3_[i] = h * k1_[i] - rc2_[i];
           rc4_[i] = rc2_[i] - h * k7_[i] - rc3_[i];
           rc5_[i] = h * (d1 * k1_[i] + d3 * k3_[i] + d4 * k4_[i] + d5 * k5_[i] + d6 * k6_[i] +
                          d7 * k7_[i]);
-        }
+        });
         t_old_ = t_;
-        y_old_ = y_;
+        y_old_.swap(y_);  // y_old = y; y = ysti (ysti is rewritten before its next read)
         t_ += h;
         h_last_ = h;
-        y_ = ysti_;
+        y_.swap(ysti_);
         k1_.swap(k7_);
         ++steps;
         if (!clamped) h_ = h_new;
@@ -635,8 +768,10 @@ class Dopri5 {
   void dense(double t, Vec& out) const {  // :150-154
     const double theta = (t - t_old_) / h_last_;
     const double th1 = 1.0 - theta;
-    for (size_t i = 0; i < out.size(); ++i)
-      out[i] = rc1_[i] + theta * (rc2_[i] + th1 * (rc3_[i] + theta * (rc4_[i] + th1 * rc5_[i])));
+    par_for(out.size(), [&](size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; ++i)
+        out[i] = rc1_[i] + theta * (rc2_[i] + th1 * (rc3_[i] + theta * (rc4_[i] + th1 * rc5_[i])));
+    });
   }
 
  private:
@@ -647,13 +782,13 @@ class Dopri5 {
       const double sc = atol_ + rtol_ * std::abs(y_[i]);
       d0 += std::norm(y_[i] / sc);
       d1n += std::norm(k1_[i] / sc);
-    }
+    }  // once per solve: left sequential
     d0 = std::sqrt(d0 / static_cast<double>(n));
     d1n = std::sqrt(d1n / static_cast<double>(n));
     double h0 = (d0 < 1e-5 || d1n < 1e-5) ? 1e-6 : 0.01 * d0 / d1n;
     h0 = std::min(h0, t_end - t_);
     if (!(h0 > 0)) h0 = 1e-6;
-    for (size_t i = 0; i < n; ++i) ysti_[i] = y_[i] + h0 * k1_[i];
+    PAR(ysti_[i] = y_[i] + h0 * k1_[i]);
     rhs_(t_ + h0, ysti_, k2_);
     ++rhs_evals_;
     double d2 = 0.0;
@@ -674,6 +809,7 @@ class Dopri5 {
   long rhs_evals_ = 0;
   Vec y_, y_old_, k1_, k2_, k3_, k4_, k5_, k6_, k7_, ysti_;
   Vec rc1_, rc2_, rc3_, rc4_, rc5_;
+  std::vector<double> q2_;
 };
 
 struct ObsEvent {
@@ -845,9 +981,11 @@ SolveResult mesolve(const TdOp& h_or_l, const QObj& rho0_in, std::span<const dou
   Vec y0(m0.v.begin(), m0.v.end());  // column stacking == column-major storage (:274-277)
   Dense rho_buf(d, d);
   integrate_events(gen, y0, tlist, saveat, opt, res.stats, [&](const ObsEvent& ev, const Vec& y) {
-    for (long j = 0; j < d; ++j)  // :286 hermitize
-      for (long i = 0; i < d; ++i)
-        rho_buf(i, j) = 0.5 * (y[static_cast<size_t>(j * d + i)] + std::conj(y[static_cast<size_t>(i * d + j)]));
+    par_for(static_cast<size_t>(d), [&](size_t lo, size_t hi) {  // :286 hermitize
+      for (long j = static_cast<long>(lo); j < static_cast<long>(hi); ++j)
+        for (long i = 0; i < d; ++i)
+          rho_buf(i, j) = 0.5 * (y[static_cast<size_t>(j * d + i)] + std::conj(y[static_cast<size_t>(i * d + j)]));
+    }, 64);
     if (ev.grid_idx >= 0)
       for (size_t e = 0; e < e_mats.size(); ++e) {  // :288-295
         cd acc = 0.0;

@@ -198,6 +198,22 @@ struct SolveResult {
 };
 
 /// evolve.hpp:96-111 / evolve.cpp:53-69
+// Worker threads for the element-wise loops and row-parallel SpMV of a single solve
+// (bench.py's reference arm: "all the host threads it can use"). Every result is bit-identical
+// to the 1-thread run: element-wise expressions are unchanged, each SpMV row accumulates its
+// entries in the same ascending-column order as the CSC scatter, and every reduction (error
+// norm, initial-step norms) is still summed sequentially in index order. Default 1.
+void set_threads(int n);
+int threads();
+
+// Row-major copy of a Csc (columns ascending within a row) for the row-parallel product.
+struct CsrRows {
+  long rows = 0;
+  std::vector<long> ptr;
+  std::vector<int> col;
+  std::vector<cd> val;
+};
+
 class SparseGenerator {
  public:
   SparseGenerator() = default;
@@ -211,6 +227,9 @@ class SparseGenerator {
   std::vector<std::pair<Csc, CoeffFn>> terms_;
   Params params_;
   mutable std::vector<cd> tmp_;
+  // threads() > 1 at construction: row-major copies used by apply()
+  CsrRows const_rows_;
+  std::vector<CsrRows> term_rows_;
 };
 
 SolveResult sesolve(const TdOp& h, const QObj& psi0, std::span<const double> tlist,

@@ -70,7 +70,7 @@ class _Stats(C.Structure):
 
 class _Timing(C.Structure):
     _fields_ = [("kernel_ms", C.c_double), ("total_ms", C.c_double), ("attempts", C.c_int64),
-                ("grid_ctas", C.c_int32), ("lanes", C.c_int32)]
+                ("grid_ctas", C.c_int32), ("lanes", C.c_int32), ("store", C.c_int32), ("reserved", C.c_int32)]
 
 
 class _McOut(C.Structure):
@@ -319,7 +319,7 @@ def _solve(fn, ctx, gen, d, y0, tlist, e_ops, params, abstol, reltol, max_steps,
         "states": None if states is None else states.reshape(nsave, n_state),
         "kernel_ms": tm.kernel_ms,
         "attempts": tm.attempts,
-        "grid_ctas": tm.grid_ctas,
+        "grid_ctas": tm.grid_ctas, "store": tm.store,
         "lanes": tm.lanes,
     }
 
@@ -649,3 +649,17 @@ def op_storage(op: "Operator"):
     L.qsg_op_dict_size.restype = C.c_int32
     L.qsg_op_dict_size.argtypes = [P]
     return L.qsg_op_code_bytes(op._h), L.qsg_op_dict_size(op._h)
+
+
+STORE_NAMES = {0: "plain", 1: "coded8", 2: "coded16", 3: "key-aligned"}
+
+
+def op_store_info(op: "Operator") -> dict:
+    """qsg_op_store_info: the stores an operator carries and the bytes one SpMV reads from each."""
+    L = lib()
+    L.qsg_op_store_info.argtypes = [P, I64P]
+    v = (C.c_int64 * 8)()
+    _check(L.qsg_op_store_info(op._h, v))
+    return {"store": STORE_NAMES[int(v[0])], "plain_bytes": int(v[1]), "coded_bytes": int(v[2]),
+            "ka_bytes": int(v[3]), "ka_values": int(v[4]), "ka_positions": int(v[5]), "coded_pairs": int(v[6]),
+            "ka_slot_bytes": int(v[7])}

@@ -290,16 +290,10 @@ extern "C" qsg_status qsg_mcsolve(qsg_ctx* ctx, const qsg_generator* G, int32_t 
       if (out->traj_stats)
         for (int k = 0; k < 3; ++k) out->traj_stats[3 * i + k] = o.stats[3 * i + k];
       if (out->jump_count) out->jump_count[i] = o.jcount[i];
+      // the device records min(jcount, run_cap) >= min(jcount, cap) jumps; jump_count keeps the full
+      // count, so a caller whose buffer was too small sees jump_count > jump_capacity and re-calls
       const double* jt = o.jtime.data() + i * run_cap;
       const int* jc = o.jch.data() + i * run_cap;
-      RunOut o1;  // a jump log longer than the device buffer: re-run this trajectory alone
-      if (o.jcount[i] > run_cap && cap > run_cap) {
-        BatchProblem P1 = P;
-        P1.sys_begin = traj_begin + i;
-        if (qsg_status st = run_batch(ctx, P1, 1, o.jcount[i], o1)) return st;
-        jt = o1.jtime.data();
-        jc = o1.jch.data();
-      }
       const int nstore = std::min(cap, o.jcount[i]);
       for (int j = 0; j < nstore; ++j) {
         if (out->jump_time) out->jump_time[i * cap + j] = jt[j];

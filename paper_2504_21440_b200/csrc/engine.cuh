@@ -39,7 +39,19 @@ struct DevSell {
   // plain store small enough that each SM's share of it stays in L1 across passes: its (col, val)
   // entries are loaded through the L1-allocating read-only path instead of L1::no_allocate
   int l1;
+  // Key-aligned store (ka_nval 0 = absent). Slice s is one block of 16-byte words at
+  // ka_blk + ka_off[s]: header {npos, nnon, 0, 0}, then npos position records {key, lane mask,
+  // value id | kKaNonUniform, exception offset}, then nnon arrays of 32 uint16 per-lane value ids.
+  // Position p holds, for every lane (row) whose mask bit is set, the entry in column row ^ key;
+  // positions are in ascending key order. Values come from the ka_val table of distinct values.
+  const unsigned* ka_off;
+  const uint4* ka_blk;
+  const double2* ka_val;
+  int ka_nval;
+  int ka_slot;  // largest block in bytes (ring slot size)
 };
+
+constexpr unsigned kKaNonUniform = 0xffffffffu;
 
 struct DevCoeff {
   int kind;  // qsg_coeff_kind
@@ -334,6 +346,39 @@ __device__ __forceinline__ double2 ld_na_c2(const double2* p) {
   asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
+
+// ---- bulk asynchronous copies (TMA engine, cp.async.bulk) completing on an mbarrier ------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// One elected thread: expect `bytes` on `bar`, then copy them global -> shared through the async
+// proxy; the copy's completion flips the barrier's phase. dst, src and bytes are 16-byte multiples.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// generic-proxy reads of a buffer before the async proxy overwrites it
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ---- block reduction (deterministic order) ----------------------------------------------------
 // Returns the block total on every thread. smem needs blockDim/32 doubles.

@@ -182,11 +182,96 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// Key-aligned store stream of one warp (ST == 2). The warp's slices b0, b0+W, ... (cnt of them) are
+// re-read in the same order by every stage pass, so their blocks form one endless stream that a
+// 2-slot ring in shared memory prefetches through the TMA engine (cp.async.bulk + mbarrier): the
+// block of stream position u lands in slot u & 1, on that slot's (u >> 1)-th barrier phase. Two
+// blocks are always in flight, across pass and grid-barrier boundaries too (the store is
+// read-only); the kernel drains them before it exits. Lane j caches the block bounds of sequence
+// index cbase + j, so issuing a copy costs two shuffles, not a dependent global load.
+struct KaRing {
+  uint4* base;               // slot 0; slot 1 at base + slot_words
+  unsigned long long* bar;   // this warp's two mbarriers
+  const uint4* blk;          // store blocks (global)
+  const unsigned* off;       // block offsets (global, 16-byte units)
+  int slot_words, b0, W, cnt, cbase;
+  unsigned used, issued;     // stream positions (identical in every lane)
+  unsigned off_lo, off_hi;   // lane j: bounds of sequence index cbase + j
+
+  __device__ __forceinline__ void refill(int k) {
+    cbase = k & ~31;
+    const int j = cbase + (threadIdx.x & 31);
+    if (j < cnt) {
+      const int b = b0 + j * W;
+      off_lo = __ldg(off + b);
+      off_hi = __ldg(off + b + 1);
+    }
+  }
+  __device__ __forceinline__ void issue() {
+    const int k = static_cast<int>(issued % static_cast<unsigned>(cnt));
+    if (k < cbase || k >= cbase + 32) refill(k);
+    const unsigned lo = __shfl_sync(0xffffffffu, off_lo, k - cbase);
+    const unsigned hi = __shfl_sync(0xffffffffu, off_hi, k - cbase);
+    if ((threadIdx.x & 31) == 0) {
+      const unsigned sl = issued & 1u;
+      bulk_g2s(base + sl * slot_words, blk + lo, 16u * (hi - lo), bar + sl);
+    }
+    ++issued;
+  }
+  __device__ __forceinline__ const uint4* wait() {
+    const unsigned sl = used & 1u;
+    mbar_wait(bar + sl, (used >> 1) & 1u);
+    return base + sl * slot_words;
+  }
+  // every lane is done reading the current slot: hand it to the async proxy for position used + 2
+  __device__ __forceinline__ void release() {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) fence_proxy_async();
+    ++used;
+    issue();
+  }
+};
+
+// One slice of the key-aligned store from its staged block: for every position (ascending key) the
+// lanes whose mask bit is set gather x[row ^ key] and multiply by the position's value: one
+// warp-uniform shared-memory word per position, plus per-lane value ids where the position's values
+// differ across lanes (the diagonal, typically).
+template <class XF>
+__device__ __forceinline__ double2 ka_row(const uint4* __restrict__ blk, const double2* __restrict__ vals, int row,
+                                          XF&& xf) {
+  __builtin_assume(__isShared(blk));
+  __builtin_assume(__isShared(vals));
+  const int lane = threadIdx.x & 31;
+  const unsigned bit = 1u << lane;
+  const int np = static_cast<int>(blk[0].x);
+  const unsigned short* ex = reinterpret_cast<const unsigned short*>(blk);
+  double2 acc = make_double2(0.0, 0.0);
+  const double2 z = make_double2(0.0, 0.0);
+  for (int p0 = 0; p0 < np; p0 += 4) {
+    uint4 r[4];
+    double2 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u] = p0 + u < np ? blk[1 + p0 + u] : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = (r[u].y & bit) ? xf(row ^ static_cast<int>(r[u].x)) : z;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (r[u].y & bit) {
+        const unsigned vid = r[u].z != kKaNonUniform ? r[u].z : static_cast<unsigned>(ex[r[u].w + lane]);
+        cfma(vals[vid], x[u], acc);
+      }
+  }
+  return acc;
+}
+
 // X2 (stage 2 only): the stage input y + h a21 k1 was materialised in SB by x2_pass, so the SpMV
 // gathers one vector instead of two.
-template <int S, bool PF, bool X2 = false>
+// ST: 0 generic rows, 1 coded store (software-pipelined), 2 key-aligned store through the ring.
+template <int S, int ST, bool X2 = false>
 __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c, int s0, int s1,
-                                             const double2* sval = nullptr, const int* soff = nullptr) {
+                                             const double2* sval = nullptr, const int* soff = nullptr,
+                                             KaRing* ring = nullptr) {
+  constexpr bool PF = ST >= 1;
   using namespace dp;
   const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = P.n;
@@ -218,6 +303,7 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
   };
   // streamed once per pass: do not allocate in L1, which then keeps more of the x-gather lines
   auto ldo = [](const double2* p) { return ld_na_c2(p); };
+  (void)ring;
   auto load_operands = [&](int row, bool ok, Ops& o) {
     o.yy = ok ? ldo(y + row) : z;
     o.q1 = ok ? ldo(k1 + row) : z;
@@ -267,6 +353,38 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
       esq += qq * qq;
     }
   };
+  if constexpr (ST == 2) {
+    // key-aligned store: blocks arrive through the warp's ring; sval is the value table
+    KaRing& R = *ring;
+    for (int k = 0; k < R.cnt; ++k) {
+      const int b = R.b0 + k * R.W;
+      const int row = (b << 5) + lane;
+      const bool ok = row < n;
+      const uint4* blk = R.wait();
+      const double2 kk = ka_row(blk, sval, row, xin);
+      R.release();
+      const int bn = b + R.W;
+      if (bn < s1) {
+        const int rn = (bn << 5) + lane;
+        if (rn < n) {
+          prefetch_l2(y + rn);
+          prefetch_l2(k1 + rn);
+          if (S >= 3 && S <= 5) prefetch_l2(pk2 + rn);
+          if (S >= 4) prefetch_l2(pk3 + rn);
+          if (S >= 5) prefetch_l2(pk4 + rn);
+          if (S >= 6) prefetch_l2(pk5 + rn);
+          if (S == 7) {
+            prefetch_l2(pk6 + rn);
+            prefetch_l2(x + rn);
+          }
+        }
+      }
+      Ops o;
+      load_operands(row, ok, o);
+      if (ok) epilogue(row, kk, o);
+    }
+    return esq;
+  }
   if constexpr (PF) {
     if (P.gen.n_terms == 1) {
       // Software-pipelined coded SpMV: the next slice's row metadata is loaded at the top of the
@@ -457,8 +575,9 @@ __device__ void finish_attempt(const GridProblem& P, Ctl& c, double err_sq, int 
   }
 }
 
-template <int MODE, bool PF>
+template <int MODE, int ST>
 __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const __grid_constant__ GridProblem P) {
+  constexpr bool PF = ST >= 1;
   __shared__ double s_red[kThreads / 32];
   __shared__ double s_val[2];
   __shared__ Ctl c;
@@ -502,7 +621,39 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
   // dictionary of a single-term coded generator staged in shared memory (P.smem_dict entries)
   const double2* sval = nullptr;
   const int* soff = nullptr;
-  if (PF && P.smem_dict > 0) {
+  KaRing ring{};
+  if constexpr (ST == 2) {
+    // value table, then one 2-slot ring and two mbarriers per warp (layout of dict_smem_bytes)
+    const DevSell& A = P.gen.A[0];
+    double2* vt = reinterpret_cast<double2*>(s_dyn);
+    for (int i = threadIdx.x; i < A.ka_nval; i += blockDim.x) vt[i] = A.ka_val[i];
+    const int W = blockDim.x >> 5, warp = threadIdx.x >> 5;
+    const int sw = A.ka_slot / 16;
+    uint4* rings = reinterpret_cast<uint4*>(vt + A.ka_nval);
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(rings + 2 * sw * W);
+    ring.base = rings + 2 * sw * warp;
+    ring.bar = bars + 2 * warp;
+    ring.blk = A.ka_blk;
+    ring.off = A.ka_off;
+    ring.slot_words = sw;
+    ring.b0 = s0 + warp;
+    ring.W = W;
+    ring.cnt = ring.b0 < s1 ? (s1 - ring.b0 + W - 1) / W : 0;
+    ring.cbase = -64;
+    ring.used = ring.issued = 0;
+    if ((threadIdx.x & 31) == 0) {
+      mbar_init(ring.bar, 1);
+      mbar_init(ring.bar + 1, 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+    if (ring.cnt > 0) {
+      ring.issue();
+      ring.issue();
+    }
+    sval = vt;
+  }
+  if (ST == 1 && P.smem_dict > 0) {
     const DevSell& A = P.gen.A[0];
     double2* dv = reinterpret_cast<double2*>(s_dyn);
     int* dof = reinterpret_cast<int*>(dv + P.smem_dict);
@@ -578,9 +729,9 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     if (PF && P.x2) {
       x2_pass(P, c, s0, s1);
       grid_barrier(P.bar, G);
-      stage_pass<2, PF, true>(P, c, s0, s1, sval, soff);
+      stage_pass<2, ST, true>(P, c, s0, s1, sval, soff, &ring);
     } else {
-      stage_pass<2, PF>(P, c, s0, s1, sval, soff);
+      stage_pass<2, ST == 2 ? 1 : ST>(P, c, s0, s1, sval, soff, &ring);
     }
     if (c.np) observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
     grid_barrier(P.bar, G);
@@ -592,15 +743,15 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
         c.np = 0;
       }
     }
-    stage_pass<3, PF>(P, c, s0, s1, sval, soff);
+    stage_pass<3, ST>(P, c, s0, s1, sval, soff, &ring);
     grid_barrier(P.bar, G);
-    stage_pass<4, PF>(P, c, s0, s1, sval, soff);
+    stage_pass<4, ST>(P, c, s0, s1, sval, soff, &ring);
     grid_barrier(P.bar, G);
-    stage_pass<5, PF>(P, c, s0, s1, sval, soff);
+    stage_pass<5, ST>(P, c, s0, s1, sval, soff, &ring);
     grid_barrier(P.bar, G);
-    stage_pass<6, PF>(P, c, s0, s1, sval, soff);
+    stage_pass<6, ST>(P, c, s0, s1, sval, soff, &ring);
     grid_barrier(P.bar, G);
-    double esq = stage_pass<7, PF>(P, c, s0, s1, sval, soff);
+    double esq = stage_pass<7, ST>(P, c, s0, s1, sval, soff, &ring);
     esq = block_sum(esq, s_red);
     if (threadIdx.x == 0) red[static_cast<long long>(kSlotErr) * G + rank] = esq;
     grid_barrier(P.bar, G);
@@ -631,6 +782,13 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
       flush_obs();
     }
   }
+  if constexpr (ST == 2) {  // the two blocks still in flight land before the CTA exits
+    if (ring.cnt > 0) {
+      ring.wait();
+      ++ring.used;
+      ring.wait();
+    }
+  }
   if (rank == 0 && threadIdx.x == 0) {
     GridCtl* o = P.ctl;
     o->t = c.t;
@@ -645,21 +803,19 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
   }
 }
 
-size_t dict_smem_bytes(const GridProblem& P) {
-  return static_cast<size_t>(P.smem_dict) * (sizeof(double2) + sizeof(int));
-}
-
-template <int MODE, bool PF>
+template <int MODE, int ST>
 cudaError_t launch_one(const GridProblem& P, int grid, cudaStream_t s) {
   void* args[] = {const_cast<GridProblem*>(&P)};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dp5_grid_kernel<MODE, PF>), dim3(grid),
-                                     dim3(kThreads), args, dict_smem_bytes(P), s);
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dp5_grid_kernel<MODE, ST>), dim3(grid),
+                                     dim3(kThreads), args, grid_smem_bytes(P, ST), s);
 }
 
-template <int MODE, bool PF>
+template <int MODE, int ST>
 int occupancy_one(size_t smem) {
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp5_grid_kernel<MODE, PF>, kThreads, smem);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(dp5_grid_kernel<MODE, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp5_grid_kernel<MODE, ST>, kThreads, smem);
   return nb;
 }
 
@@ -667,14 +823,26 @@ int occupancy_one(size_t smem) {
 
 int grid_threads() { return kThreads; }
 
-int grid_max_blocks_per_sm(int mode, bool pf, size_t dyn_smem) {
-  if (mode == 0) return pf ? occupancy_one<0, true>(dyn_smem) : occupancy_one<0, false>(dyn_smem);
-  return pf ? occupancy_one<1, true>(dyn_smem) : occupancy_one<1, false>(dyn_smem);
+size_t grid_smem_bytes(const GridProblem& P, int st) {
+  if (st == 2) {
+    const DevSell& A = P.gen.A[0];
+    const int W = kThreads / 32;
+    return static_cast<size_t>(A.ka_nval) * sizeof(double2) + static_cast<size_t>(2 * W) * A.ka_slot +
+           static_cast<size_t>(2 * W) * sizeof(unsigned long long);
+  }
+  return static_cast<size_t>(P.smem_dict) * (sizeof(double2) + sizeof(int));
 }
 
-cudaError_t launch_grid_dp5(const GridProblem& P, int mode, bool pf, int grid, cudaStream_t s) {
-  if (mode == 0) return pf ? launch_one<0, true>(P, grid, s) : launch_one<0, false>(P, grid, s);
-  return pf ? launch_one<1, true>(P, grid, s) : launch_one<1, false>(P, grid, s);
+int grid_max_blocks_per_sm(int mode, int st, size_t dyn_smem) {
+  if (mode == 0)
+    return st == 2 ? occupancy_one<0, 2>(dyn_smem) : st == 1 ? occupancy_one<0, 1>(dyn_smem) : occupancy_one<0, 0>(dyn_smem);
+  return st == 2 ? occupancy_one<1, 2>(dyn_smem) : st == 1 ? occupancy_one<1, 1>(dyn_smem) : occupancy_one<1, 0>(dyn_smem);
+}
+
+cudaError_t launch_grid_dp5(const GridProblem& P, int mode, int st, int grid, cudaStream_t s) {
+  if (mode == 0)
+    return st == 2 ? launch_one<0, 2>(P, grid, s) : st == 1 ? launch_one<0, 1>(P, grid, s) : launch_one<0, 0>(P, grid, s);
+  return st == 2 ? launch_one<1, 2>(P, grid, s) : st == 1 ? launch_one<1, 1>(P, grid, s) : launch_one<1, 0>(P, grid, s);
 }
 
 }  // namespace qsg

@@ -53,7 +53,9 @@ struct GridProblem {
 };
 
 int grid_threads();
-int grid_max_blocks_per_sm(int mode, bool pf, size_t dyn_smem = 0);
-cudaError_t launch_grid_dp5(const GridProblem& P, int mode, bool pf, int grid, cudaStream_t s);
+// st: 0 generic rows, 1 dictionary-coded store (pipelined), 2 key-aligned store (TMA ring)
+size_t grid_smem_bytes(const GridProblem& P, int st);
+int grid_max_blocks_per_sm(int mode, int st, size_t dyn_smem = 0);
+cudaError_t launch_grid_dp5(const GridProblem& P, int mode, int st, int grid, cudaStream_t s);
 
 }  // namespace qsg

@@ -2,6 +2,7 @@
 // (evolve.cpp:191-299, trajectories.cpp:217-249), uploads it into the HBM operator store and
 // runs the device engines through the C-ABI (include/qsg.h). No CPU integration path exists.
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -367,7 +368,13 @@ TrajectoryEnsembleResult mcsolve(const TimeDependentOperator& h, const QuantumOb
   const qsg_solve_opts o = to_opts(options);
   std::vector<int> devs = ens.devices.empty() ? std::vector<int>{options.device} : ens.devices;
   const int nd = static_cast<int>(std::min<long>(static_cast<long>(devs.size()), ntraj));
-  constexpr long kJumpCap = 256;
+  // jump records kept per trajectory by the batched call; longer logs are re-run below
+  // (QSG_MC_JUMP_CAP lowers the capacity so tests can exercise that path)
+  const long kJumpCap = [] {
+    const char* e = std::getenv("QSG_MC_JUMP_CAP");
+    const long v = e ? std::atol(e) : 0;
+    return v > 0 ? v : 256L;
+  }();
   std::vector<Complex> per(static_cast<size_t>(ntraj * blk));
   std::vector<int32_t> failed(static_cast<size_t>(ntraj)), jcount(static_cast<size_t>(ntraj));
   std::vector<double> ftime(static_cast<size_t>(ntraj)), jtime(static_cast<size_t>(ntraj * kJumpCap));
@@ -449,8 +456,38 @@ TrajectoryEnsembleResult mcsolve(const TimeDependentOperator& h, const QuantumOb
   for (int i : r.traj_indices) {
     std::vector<JumpEvent> jr;
     const int cnt = jcount[static_cast<size_t>(i)];
-    for (int j = 0; j < cnt && j < kJumpCap; ++j)
-      jr.push_back({jtime[static_cast<size_t>(i * kJumpCap + j)], jch[static_cast<size_t>(i * kJumpCap + j)]});
+    if (cnt > kJumpCap) {
+      // more jumps than the batch buffers hold: re-run trajectory i alone (it always uses
+      // RngStream(seed, i), so the re-run is the same trajectory) with room for every jump, as the
+      // reference keeps the whole list (trajectories.cpp:189-200)
+      std::vector<double> t1(static_cast<size_t>(cnt));
+      std::vector<int32_t> c1(static_cast<size_t>(cnt));
+      std::vector<Complex> p1(static_cast<size_t>(std::max<long>(1, blk))), b1(p1.size());
+      int32_t f1 = 0, n1 = 0;
+      double ft1 = 0.0;
+      int64_t ok1 = 0, st1[3] = {0, 0, 0};
+      qsg_mc_out out{};
+      out.per_traj_expect = reinterpret_cast<double*>(p1.data());
+      out.block_sum = reinterpret_cast<double*>(b1.data());
+      out.n_ok = &ok1;
+      out.failed = &f1;
+      out.fail_time = &ft1;
+      out.traj_stats = st1;
+      out.jump_count = &n1;
+      out.jump_time = t1.data();
+      out.jump_channel = c1.data();
+      out.jump_capacity = cnt;
+      qsg_ctx* ctx = device_ctx(devs[0]);
+      DeviceGenerator gen(ctx, heff, Complex(0, -1));
+      check(qsg_mcsolve(ctx, &gen.g, static_cast<int32_t>(cv.size()), cv.data(), static_cast<int32_t>(ne), ev.data(),
+                        psi0.dim(), reinterpret_cast<const double*>(y0.data()), tlist.data(), nt, params.data(),
+                        static_cast<int32_t>(params.size()), ens.seed, i, i + 1, &o, &out, nullptr));
+      require(n1 == cnt, ErrorCode::EnsembleFailure, "jump log re-run diverged");
+      for (int j = 0; j < cnt; ++j) jr.push_back({t1[static_cast<size_t>(j)], c1[static_cast<size_t>(j)]});
+    } else {
+      for (int j = 0; j < cnt; ++j)
+        jr.push_back({jtime[static_cast<size_t>(i * kJumpCap + j)], jch[static_cast<size_t>(i * kJumpCap + j)]});
+    }
     r.jump_records.push_back(std::move(jr));
     if (ens.store_per_traj) r.per_traj_expect.push_back(mats[static_cast<size_t>(i)]);
   }

@@ -213,6 +213,17 @@ struct DevCsrBuf {
   }
 };
 
+// 64-bit total of the per-row counts: the int32 scan below would wrap silently past 2^31 entries
+__global__ void count_total_kernel(const int* __restrict__ cnt, long long n, unsigned long long* total) {
+  unsigned long long a = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    a += static_cast<unsigned>(cnt[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(total, a);
+}
+
 // Assembles L into device CSR arrays owned by the caller-provided buffers.
 qsg_status assemble(qsg_ctx* ctx, int64_t d, const qsg_csr* H, int32_t n_c, const qsg_csr* c_ops, DevBuf& rp,
                     DevBuf& col, DevBuf& val, long long& nnz) {
@@ -283,6 +294,21 @@ qsg_status assemble(qsg_ctx* ctx, int64_t d, const qsg_csr* H, int32_t n_c, cons
   liouvillian_kernel<false><<<blocks, 256, 0, s>>>(P);
   if ((e = cudaGetLastError())) return cuda_fail(e, "Liouvillian count");
   cudaMemsetAsync(rp.as<int>() + n, 0, sizeof(int), s);
+  {
+    DevBuf tot;
+    unsigned long long total64 = 0;
+    if ((e = tot.alloc(sizeof(unsigned long long), s))) return cuda_fail(e, "Liouvillian count");
+    cudaMemsetAsync(tot.p, 0, sizeof(unsigned long long), s);
+    count_total_kernel<<<blocks, 256, 0, s>>>(rp.as<int>(), n, tot.as<unsigned long long>());
+    if ((e = cudaGetLastError()) ||
+        (e = cudaMemcpyAsync(&total64, tot.p, sizeof(total64), cudaMemcpyDeviceToHost, s)) ||
+        (e = cudaStreamSynchronize(s)))
+      return cuda_fail(e, "Liouvillian count");
+    if (total64 > 0x7fffffffULL) {  // before any entry buffer is sized or written
+      set_error("TooLarge: Liouvillian nnz exceeds int32 indexing");
+      return QSG_TOO_LARGE;
+    }
+  }
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, rp.as<int>(), rp.as<int>(), static_cast<int>(n + 1), s);
   DevBuf tmp;

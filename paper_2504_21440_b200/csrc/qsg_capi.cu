@@ -61,6 +61,11 @@ DevSell sell_view(const qsg_op* op, bool use_codes) {
   const char* l1e = std::getenv("QSG_L1OP_MAX_BYTES");
   const long long l1_max = l1e ? std::atoll(l1e) : (64LL << 20);
   v.l1 = v.code_bytes == 0 && 20 * op->nnz <= l1_max;
+  v.ka_off = op->ka_off;
+  v.ka_blk = op->ka_blk;
+  v.ka_val = op->ka_val;
+  v.ka_nval = use_codes ? op->ka_nval : 0;
+  v.ka_slot = op->ka_slot;
   return v;
 }
 
@@ -240,12 +245,14 @@ __device__ __forceinline__ unsigned long long pair_sig(int off, unsigned long lo
   return h | 1ull;
 }
 
+// VALUE_ONLY: key on the value alone (the key-aligned store's table of distinct values)
+template <bool VALUE_ONLY = false>
 __global__ void dict_claim_kernel(const int* rowptr, const int* col, const double2* val, int n,
                                   unsigned long long* tsig, int* toff, double2* tval, int* overflow) {
   const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n) return;
   for (int p = rowptr[r]; p < rowptr[r + 1]; ++p) {
-    const int off = col[p] - static_cast<int>(r);
+    const int off = VALUE_ONLY ? 0 : col[p] - static_cast<int>(r);
     const double2 v = val[p];
     const unsigned long long sg =
         pair_sig(off, __double_as_longlong(v.x), __double_as_longlong(v.y));
@@ -269,13 +276,14 @@ __global__ void dict_claim_kernel(const int* rowptr, const int* col, const doubl
   }
 }
 
+template <bool VALUE_ONLY = false>
 __global__ void dict_lookup_kernel(const int* rowptr, const int* col, const double2* val, int n,
                                    const unsigned long long* tsig, const int* toff, const double2* tval,
                                    unsigned* slot_of, int* overflow) {
   const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n) return;
   for (int p = rowptr[r]; p < rowptr[r + 1]; ++p) {
-    const int off = col[p] - static_cast<int>(r);
+    const int off = VALUE_ONLY ? 0 : col[p] - static_cast<int>(r);
     const double2 v = val[p];
     const unsigned long long re = __double_as_longlong(v.x), im = __double_as_longlong(v.y);
     const unsigned long long sg = pair_sig(off, re, im);
@@ -357,9 +365,9 @@ static cudaError_t build_coded_store(qsg_op* op, const int* rp, const int* col, 
   cudaMemsetAsync(tsig.p, 0, sizeof(unsigned long long) * kDictSlots, s);
   cudaMemsetAsync(ovf.p, 0, sizeof(int), s);
   const unsigned nb = static_cast<unsigned>((n + 255) / 256);
-  dict_claim_kernel<<<nb, 256, 0, s>>>(rp, col, val, static_cast<int>(n), tsig.as<unsigned long long>(),
+  dict_claim_kernel<false><<<nb, 256, 0, s>>>(rp, col, val, static_cast<int>(n), tsig.as<unsigned long long>(),
                                        toff.as<int>(), tval.as<double2>(), ovf.as<int>());
-  dict_lookup_kernel<<<nb, 256, 0, s>>>(rp, col, val, static_cast<int>(n), tsig.as<unsigned long long>(),
+  dict_lookup_kernel<false><<<nb, 256, 0, s>>>(rp, col, val, static_cast<int>(n), tsig.as<unsigned long long>(),
                                         toff.as<int>(), tval.as<double2>(), slot_of.as<unsigned>(), ovf.as<int>());
   dict_compact_kernel<<<1, 1024, 0, s>>>(tsig.as<unsigned long long>(), toff.as<int>(), tval.as<double2>(),
                                          dense.as<unsigned>(), doff.as<int>(), dval.as<double2>(), 65536,
@@ -394,6 +402,157 @@ static cudaError_t build_coded_store(qsg_op* op, const int* rp, const int* col, 
   if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(s))) return e;
   op->code_bytes = cbytes;
   op->dict_n = count;
+  return cudaSuccess;
+}
+
+
+// ---- key-aligned store, built on the device -------------------------------------
+// One warp per 32-row slice. Each lane sorts its row's entries by key = col ^ row; the warp then
+// merges the 32 sorted lists: position p takes the warp-minimum head key, the lanes holding it set
+// their bit in the position's lane mask and advance. A position whose lanes all carry the same
+// value (bit-exact) stores that value's id once (warp-uniform); otherwise it stores one uint16 id
+// per lane. COUNT pass: widths (npos, nnon) per slice; FILL pass: the blocks.
+constexpr int kKaMaxRow = 64;   // longest row the per-lane sort handles
+constexpr int kKaMaxPos = 128;  // widest key union per slice
+constexpr int kKaMaxVals = 2048;
+
+template <bool FILL>
+__global__ void __launch_bounds__(128) ka_slice_kernel(const int* __restrict__ rowptr, const int* __restrict__ col,
+                                                       const unsigned* __restrict__ slot_of,
+                                                       const unsigned* __restrict__ dense, int n, int nsl,
+                                                       unsigned* __restrict__ npos_out, unsigned* __restrict__ nnon_out,
+                                                       const unsigned* __restrict__ off16, uint4* __restrict__ blk,
+                                                       int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= nsl) return;
+  const int r = s * 32 + lane;
+  const int b = r < n ? rowptr[r] : 0;
+  const int len = r < n ? rowptr[r + 1] - b : 0;
+  if (__any_sync(0xffffffffu, len > kKaMaxRow)) {
+    if (lane == 0) atomicExch(bad, 1);
+    return;
+  }
+  unsigned key[kKaMaxRow], vid[kKaMaxRow];
+  for (int k = 0; k < len; ++k) {  // insertion sort by key
+    const unsigned kk = static_cast<unsigned>(col[b + k]) ^ static_cast<unsigned>(r);
+    const unsigned vv = dense[slot_of[b + k]];
+    int j = k;
+    while (j > 0 && key[j - 1] > kk) {
+      key[j] = key[j - 1];
+      vid[j] = vid[j - 1];
+      --j;
+    }
+    key[j] = kk;
+    vid[j] = vv;
+  }
+  unsigned np = 0, nn = 0;
+  const unsigned npos_total = FILL ? npos_out[s] : 0;
+  uint4* out = FILL ? blk + off16[s] : nullptr;
+  unsigned short* ex = FILL ? reinterpret_cast<unsigned short*>(out + 1 + npos_total) : nullptr;
+  int h = 0;
+  for (;;) {
+    const unsigned my = h < len ? key[h] : 0xffffffffu;
+    const unsigned m = __reduce_min_sync(0xffffffffu, my);
+    if (m == 0xffffffffu) break;
+    const bool has = my == m;
+    const unsigned mask = __ballot_sync(0xffffffffu, has);
+    const unsigned v = has ? vid[h] : 0u;
+    const unsigned vmin = __reduce_min_sync(0xffffffffu, has ? v : 0xffffffffu);
+    const unsigned vmax = __reduce_max_sync(0xffffffffu, has ? v : 0u);
+    const bool uni = vmin == vmax;
+    if (FILL) {
+      if (!uni) ex[32 * nn + lane] = static_cast<unsigned short>(v);
+      if (lane == 0)
+        out[1 + np] = make_uint4(m, mask, uni ? vmin : kKaNonUniform, uni ? 0u : 8u * (1u + npos_total) + 32u * nn);
+    }
+    ++np;
+    nn += uni ? 0u : 1u;
+    if (has) ++h;
+  }
+  if (lane == 0) {
+    if (FILL) {
+      out[0] = make_uint4(np, nn, 0u, 0u);
+    } else {
+      npos_out[s] = np;
+      nnon_out[s] = nn;
+    }
+  }
+}
+
+// Builds the key-aligned store of `op` from the staged CSR when it pays: at most kKaMaxVals
+// distinct values, rows of at most kKaMaxRow entries, and key unions no wider than 1.25x the
+// entries (lane slots 32 * sum(npos) <= 1.25 nnz). Otherwise op keeps its other stores.
+static cudaError_t build_ka_store(qsg_op* op, const int* rp, const int* col, const double2* val, long long n,
+                                  cudaStream_t s) {
+  const long long nsl = (n + 31) / 32;
+  cudaError_t e;
+  DevBuf tsig, toff, tval, slot_of, dense, cnt, ovf, doff, dval, dnp, dnn, doff16, dbad;
+  if ((e = tsig.alloc(sizeof(unsigned long long) * kDictSlots, s)) || (e = toff.alloc(sizeof(int) * kDictSlots, s)) ||
+      (e = tval.alloc(sizeof(double2) * kDictSlots, s)) || (e = slot_of.alloc(sizeof(unsigned) * op->nnz, s)) ||
+      (e = dense.alloc(sizeof(unsigned) * kDictSlots, s)) || (e = cnt.alloc(sizeof(int), s)) ||
+      (e = ovf.alloc(sizeof(int), s)) || (e = doff.alloc(sizeof(int) * kKaMaxVals, s)) ||
+      (e = dval.alloc(sizeof(double2) * kKaMaxVals, s)) || (e = dnp.alloc(sizeof(unsigned) * nsl, s)) ||
+      (e = dnn.alloc(sizeof(unsigned) * nsl, s)) || (e = dbad.alloc(sizeof(int), s)))
+    return e;
+  cudaMemsetAsync(tsig.p, 0, sizeof(unsigned long long) * kDictSlots, s);
+  cudaMemsetAsync(ovf.p, 0, sizeof(int), s);
+  cudaMemsetAsync(dbad.p, 0, sizeof(int), s);
+  const unsigned nb = static_cast<unsigned>((n + 255) / 256);
+  dict_claim_kernel<true><<<nb, 256, 0, s>>>(rp, col, val, static_cast<int>(n), tsig.as<unsigned long long>(),
+                                             toff.as<int>(), tval.as<double2>(), ovf.as<int>());
+  dict_lookup_kernel<true><<<nb, 256, 0, s>>>(rp, col, val, static_cast<int>(n), tsig.as<unsigned long long>(),
+                                              toff.as<int>(), tval.as<double2>(), slot_of.as<unsigned>(), ovf.as<int>());
+  dict_compact_kernel<<<1, 1024, 0, s>>>(tsig.as<unsigned long long>(), toff.as<int>(), tval.as<double2>(),
+                                         dense.as<unsigned>(), doff.as<int>(), dval.as<double2>(), kKaMaxVals,
+                                         cnt.as<int>());
+  int count = 0, overflow = 0;
+  if ((e = cudaGetLastError()) || (e = cudaMemcpyAsync(&count, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+      (e = cudaMemcpyAsync(&overflow, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, s)) || (e = cudaStreamSynchronize(s)))
+    return e;
+  if (overflow || count < 1 || count > kKaMaxVals) return cudaSuccess;
+  const unsigned kb = static_cast<unsigned>((nsl * 32 + 127) / 128);
+  ka_slice_kernel<false><<<kb, 128, 0, s>>>(rp, col, slot_of.as<unsigned>(), dense.as<unsigned>(), static_cast<int>(n),
+                                            static_cast<int>(nsl), dnp.as<unsigned>(), dnn.as<unsigned>(), nullptr,
+                                            nullptr, dbad.as<int>());
+  std::vector<unsigned> np(static_cast<size_t>(nsl)), nn(static_cast<size_t>(nsl));
+  int bad = 0;
+  if ((e = cudaGetLastError()) ||
+      (e = cudaMemcpyAsync(np.data(), dnp.p, sizeof(unsigned) * nsl, cudaMemcpyDeviceToHost, s)) ||
+      (e = cudaMemcpyAsync(nn.data(), dnn.p, sizeof(unsigned) * nsl, cudaMemcpyDeviceToHost, s)) ||
+      (e = cudaMemcpyAsync(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost, s)) || (e = cudaStreamSynchronize(s)))
+    return e;
+  if (bad) return cudaSuccess;
+  std::vector<unsigned> off(static_cast<size_t>(nsl + 1), 0);
+  long long pos = 0, words = 0;
+  unsigned slot = 0;
+  for (long long i = 0; i < nsl; ++i) {
+    if (np[i] > static_cast<unsigned>(kKaMaxPos)) return cudaSuccess;
+    const unsigned w = 1 + np[i] + 4 * nn[i];
+    off[i] = static_cast<unsigned>(words);
+    words += w;
+    pos += np[i];
+    slot = std::max(slot, 16 * w);
+    if (words > 0xffffffffLL) return cudaSuccess;
+  }
+  off[nsl] = static_cast<unsigned>(words);
+  if (32 * pos * 4 > 5 * op->nnz) return cudaSuccess;  // union wider than 1.25x the entries
+  if ((e = cudaMallocAsync(&op->ka_off, sizeof(unsigned) * (nsl + 1), s)) ||
+      (e = cudaMallocAsync(&op->ka_blk, 16 * static_cast<size_t>(words), s)) ||
+      (e = cudaMallocAsync(&op->ka_val, sizeof(double2) * count, s)) ||
+      (e = doff16.alloc(sizeof(unsigned) * (nsl + 1), s)))
+    return e;
+  cudaMemcpyAsync(op->ka_off, off.data(), sizeof(unsigned) * (nsl + 1), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(op->ka_val, dval.p, sizeof(double2) * count, cudaMemcpyDeviceToDevice, s);
+  cudaMemsetAsync(op->ka_blk, 0, 16 * static_cast<size_t>(words), s);
+  ka_slice_kernel<true><<<kb, 128, 0, s>>>(rp, col, slot_of.as<unsigned>(), dense.as<unsigned>(), static_cast<int>(n),
+                                           static_cast<int>(nsl), dnp.as<unsigned>(), dnn.as<unsigned>(), op->ka_off,
+                                           op->ka_blk, dbad.as<int>());
+  if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(s))) return e;
+  op->ka_nval = count;
+  op->ka_slot = static_cast<int>(slot);
+  op->ka_bytes = 16 * words + 4 * (nsl + 1) + 16LL * count;
+  op->ka_positions = pos;
   return cudaSuccess;
 }
 
@@ -572,12 +731,17 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   const char* sd = std::getenv("QSG_SMEM_DICT");
   if (pf && G->n_terms == 1 && G->ops[0]->dict_n > 0 && G->ops[0]->dict_n <= 2048 && !(sd && sd[0] == '0'))
     P.smem_dict = G->ops[0]->dict_n;
-  const size_t dyn = static_cast<size_t>(P.smem_dict) * (sizeof(double2) + sizeof(int));
+  // single-term generator with a key-aligned store: stream it through the TMA ring (st 2);
+  // QSG_NO_KA_SOLVE=1 keeps the coded path
+  const char* nks = std::getenv("QSG_NO_KA_SOLVE");
+  const int st = (G->n_terms == 1 && G->ops[0]->ka_nval > 0 && !(nks && nks[0] == '1')) ? 2 : pf ? 1 : 0;
+  if (st == 2) P.smem_dict = 0;
+  const size_t dyn = grid_smem_bytes(P, st);
   // materialise the stage-2 input for the pipelined single-term path: one extra streaming pass and
   // barrier, half the stage-2 gathers (TFIM-10: 30.2 -> 29.1 ms). QSG_X2=0 disables.
-  P.x2 = pf && G->n_terms == 1;
-  if (const char* x2 = std::getenv("QSG_X2")) P.x2 = x2[0] == '1' && P.x2;
-  const int per_sm = grid_max_blocks_per_sm(mode, pf, dyn);
+  P.x2 = st >= 1 && G->n_terms == 1;
+  if (const char* x2 = std::getenv("QSG_X2")) P.x2 = (x2[0] == '1' && P.x2) || st == 2;
+  const int per_sm = grid_max_blocks_per_sm(mode, st, dyn);
   if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "occupancy");
   const int max_grid = per_sm * ctx->sm_count;
   const long long nblk = (n + 31) / 32;
@@ -596,7 +760,7 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   P.red = d_red.as<double>();
   P.bar = d_bar.as<unsigned>();
   cudaEventRecord(ctx->ev[0], s);
-  if ((ce = launch_grid_dp5(P, mode, pf, grid, s))) return cuda_fail(ce, "solver launch");
+  if ((ce = launch_grid_dp5(P, mode, st, grid, s))) return cuda_fail(ce, "solver launch");
   cudaEventRecord(ctx->ev[1], s);
   GridCtl ctl{};
   if ((ce = cudaMemcpyAsync(&ctl, d_ctl.p, sizeof(GridCtl), cudaMemcpyDeviceToHost, s)))
@@ -610,8 +774,9 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
     timing->attempts = ctl.attempts;
     timing->grid_ctas = grid;
     timing->lanes = lanes;
+    timing->store = st;
   }
-  if (qsg_status st = status_from_device(ctl.status, ctl.fail_t)) return st;
+  if (qsg_status sst = status_from_device(ctl.status, ctl.fail_t)) return sst;
   if (expect && n_e > 0)
     if ((ce = cudaMemcpyAsync(expect, d_exp.p, static_cast<size_t>(n_e) * n_t * sizeof(double2), cudaMemcpyDefault, s)))
       return cuda_fail(ce, "expect copy");
@@ -783,6 +948,15 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
       return cuda_fail(e, "coded operator store");
     }
     mark("coded");
+    // key-aligned store for the persistent grid engine (QSG_NO_KA=1 disables)
+    const char* nk = std::getenv("QSG_NO_KA");
+    if (!(nk && nk[0] == '1')) {
+      if ((e = build_ka_store(op, d_rp.as<int>(), d_col.as<int>(), d_val.as<double2>(), n, s))) {
+        qsg_op_destroy(op);
+        return cuda_fail(e, "key-aligned operator store");
+      }
+      mark("key-aligned");
+    }
   }
   *out = op;
   return QSG_OK;
@@ -795,6 +969,7 @@ void qsg_op_destroy(qsg_op* op) {
   cudaSetDevice(op->ctx->device);
   cudaStream_t s = op->ctx->stream;
   for (void* p : {op->code, static_cast<void*>(op->code_off), static_cast<void*>(op->dict_off),
+                  static_cast<void*>(op->ka_off), static_cast<void*>(op->ka_blk), static_cast<void*>(op->ka_val),
                   static_cast<void*>(op->dict_val), static_cast<void*>(op->slice_off),
                   static_cast<void*>(op->rowlen), static_cast<void*>(op->col), static_cast<void*>(op->val)})
     if (p) cudaFreeAsync(p, s);
@@ -807,6 +982,23 @@ int64_t qsg_op_nnz(const qsg_op* op) { return op ? op->nnz : 0; }
 
 int32_t qsg_op_code_bytes(const qsg_op* op) { return op ? op->code_bytes : -1; }
 int32_t qsg_op_dict_size(const qsg_op* op) { return op ? op->dict_n : -1; }
+
+qsg_status qsg_op_store_info(const qsg_op* op, int64_t* info) {
+  if (!op || !info) {
+    set_error("InvalidGrid: null argument");
+    return QSG_INVALID_GRID;
+  }
+  const long long nsl = op->n_slices;
+  info[0] = op->ka_nval > 0 ? 3 : op->code_bytes;
+  info[1] = 20 * op->nnz + 4 * op->n_rows + 8 * nsl;  // plain SELL bytes per SpMV
+  info[2] = op->code_bytes ? op->code_bytes * op->nnz + 4 * op->n_rows + 16 * nsl + 20LL * op->dict_n : 0;
+  info[3] = op->ka_bytes;
+  info[4] = op->ka_nval;
+  info[5] = op->ka_positions;
+  info[6] = op->dict_n;
+  info[7] = op->ka_slot;
+  return QSG_OK;
+}
 int64_t qsg_op_rows(const qsg_op* op) { return op ? op->n_rows : 0; }
 
 qsg_status qsg_generator_apply(qsg_ctx* ctx, const qsg_generator* g, const double* params,

@@ -42,6 +42,15 @@ struct qsg_op {
   int* dict_off = nullptr;
   double2* dict_val = nullptr;
   int dict_n = 0;
+  // key-aligned store (engine.cuh DevSell::ka_*): per-slice blocks of (key, lane mask, value id)
+  // positions + the distinct-value table; built alongside the other stores when it pays
+  unsigned* ka_off = nullptr;  // n_slices + 1, in 16-byte units
+  uint4* ka_blk = nullptr;
+  double2* ka_val = nullptr;
+  int ka_nval = 0;
+  int ka_slot = 0;            // largest block, bytes
+  long long ka_bytes = 0;     // whole store, bytes
+  long long ka_positions = 0; // sum over slices of the key-union width
 };
 
 namespace qsg {

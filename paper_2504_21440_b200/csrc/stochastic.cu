@@ -551,10 +551,18 @@ qsg_status run_sde(qsg_ctx* ctx, int mode, const qsg_generator* G, int64_t d, in
     timing->grid_ctas = grid;
     timing->lanes = 1;
   }
-  if (out->per_traj_expect) std::memcpy(out->per_traj_expect, ex.data(), sizeof(double2) * ex.size());
-  std::vector<const double2*> blocks;
-  for (long long i = 0; i < n_sys; ++i) blocks.push_back(ex.data() + nvals * i);
-  if (out->block_sum) pairwise(blocks, 0, blocks.size(), nvals, reinterpret_cast<double2*>(out->block_sum));
+  // the device slab keeps max(1, n_e) rows per trajectory; the caller's buffers hold n_e * n_t
+  // values per trajectory (nothing at all when there are no e_ops)
+  const size_t nv = static_cast<size_t>(n_e) * n_t;
+  if (nv > 0) {
+    if (out->per_traj_expect) {
+      double2* dst = reinterpret_cast<double2*>(out->per_traj_expect);
+      for (long long i = 0; i < n_sys; ++i) std::memcpy(dst + nv * i, ex.data() + nvals * i, sizeof(double2) * nv);
+    }
+    std::vector<const double2*> blocks;
+    for (long long i = 0; i < n_sys; ++i) blocks.push_back(ex.data() + nvals * i);
+    if (out->block_sum) pairwise(blocks, 0, blocks.size(), nv, reinterpret_cast<double2*>(out->block_sum));
+  }
   out->n_ok = n_sys;
   return QSG_OK;
 }
