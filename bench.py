@@ -13,9 +13,12 @@ does not shard); the sharded workload — mcsolve trajectories o
 combined with an NCCL all-gather of the per-rank pairwise block sums — is reported under
 `secondary.mcsolve` at every N.
 
-`--impl reference` times the CPU restatement of the reference (oracle/, single-threaded as the
-reference's mesolve) on a bounded sample of the same workload (the first 0.5 time units),
-extrapolated per DP5 attempt to the full solve.
+`--impl reference` times the CPU restatement of the reference (oracle/) on the same complete
+solve, with every host thread (row-parallel SpMV and element-wise loops; bit-identical to the
+single-threaded restatement, tests/test_oracle_pinning.py), rank 0 only.
+
+`--gpus N` without a torchrun environment re-launches itself under torch.distributed.run with N
+processes (one per GPU, 127.0.0.1 rendezvous).
 """
 from __future__ import annotations
 
@@ -38,6 +41,23 @@ TLIST = np.linspace(0.0, 10.0, 100)
 TFIM = (10, 1, 1.0, 0.2, 1.0, 1)       # nx, ny, Jz, hx, gamma, periodic (scenarios/ising_mc_2x3.json:5)
 TFIM_MC = (14, 1, 1.0, 0.2, 1.0, 1)
 MC_SEED = 2025
+KERR_CUTOFFS = (50, 100, 150, 200, 300, 400)
+
+# The workload every arm of the headline line reports (identical dict in both arms).
+HEADLINE_CONFIG = {
+    "workload": "mesolve dissipative TFIM chain, 10 spins, periodic (BASELINE configs[1])",
+    "liouvillian_rows": 1048576, "liouvillian_nnz": 24641536, "tlist": "linspace(0,10,100)",
+    "abstol": 1e-08, "reltol": 1e-06, "e_ops": "Sx,Sy,Sz totals", "method": "Dormand-Prince 5(4)",
+    "l2_flush": "none needed: the 7-29 MB operator store is re-read 486 times per solve, so its L2 residency "
+                "is part of the workload; the 11 state vectors (185 MB) exceed the 126 MB L2",
+}
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 def hbm_peak():
@@ -124,6 +144,16 @@ def allreduce_max(x, ws):
     return float(t.item())
 
 
+def allreduce_sum(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def csr_bytes(m):
     return m.rowptr.nbytes + m.col.nbytes + m.val.nbytes
 
@@ -182,9 +212,11 @@ def run_ours(args, ws, rank, local):
 
     # ---- roofline of the fused DP5 kernel, per launch (= per solve). Byte model of SURVEY.md §8d
     # with the operator-store term of the format actually read.
+    store_info = q.op_store_info(op)
     cb, ndict = q.op_storage(op)
-    mat_bytes = store_bytes(cb, ndict, n, nnz)
-    b_att = 6 * mat_bytes + 47 * 16 * n
+    mat_bytes = store_bytes(cb, ndict, n, nnz)  # the SpMV / start passes read the coded or plain store
+    stage_bytes = solve_store_bytes(store_info, r["store"])  # the stage passes read this one
+    b_att = 6 * stage_bytes + 47 * 16 * n
     b_init = 2 * mat_bytes + 6 * 16 * n
     alg_bytes = b_att * att + b_init
     achieved = alg_bytes / (ms_step / 1e3) / 1e9
@@ -192,7 +224,8 @@ def run_ours(args, ws, rank, local):
     tp = os.path.join(ROOT, "profiles", "dp5_grid_kernel_dram_bytes.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("coded" if cb else "plain", {}).get("dram_bytes_per_launch")
+            key = {0: "plain", 1: "coded", 2: "key_aligned"}[int(r["store"])]
+            traffic = json.load(open(tp)).get(key, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -269,11 +302,12 @@ def run_ours(args, ws, rank, local):
                                    "plain_bytes_per_spmv": mat_p}
     if e2e_L is not None:
         secondary["e2e_from_liouvillian_csr"] = e2e_L
+    cpu_legs = rank == 0 and ws == 1 and not args.no_cpu
     if not args.quick:
         secondary["kerr_sweep_spmv"] = kerr_sweep_spmv(ctx, q, torch, dev, peak)
-        secondary["kerr_cutoff_mesolve"] = kerr_cutoff_mesolve(ctx, q, peak)
-        secondary["mcsolve"] = mcsolve_sharded(args, ctx, q, torch, ws, rank)
-        secondary["param_sweep"] = param_sweep_sharded(args, ctx, q, torch, ws, rank)
+        secondary["kerr_cutoff_mesolve"] = kerr_cutoff_mesolve(ctx, q, peak, cpu=cpu_legs)
+        secondary["mcsolve"] = mcsolve_sharded(args, ctx, q, torch, ws, rank, peak, cpu=cpu_legs)
+        secondary["param_sweep"] = param_sweep_sharded(args, ctx, q, torch, ws, rank, cpu=cpu_legs)
         secondary["stochastic"] = stochastic_secondary(args, q, rank)
         secondary["sesolve_tfim20"] = sesolve_tfim20(ctx, q, peak)
     del out, y
@@ -291,23 +325,19 @@ def run_ours(args, ws, rank, local):
         "vs_baseline": None,
         "dtype": "c128",
         "data": "synthetic: reference TFIM construction (factories.cpp:204-246), all-up initial state",
-        "config": {
-            "workload": "mesolve dissipative TFIM chain, 10 spins, periodic (BASELINE configs[1])",
-            "liouvillian_rows": n, "liouvillian_nnz": nnz, "tlist": "linspace(0,10,100)",
-            "abstol": 1e-8, "reltol": 1e-6, "e_ops": "Sx,Sy,Sz totals", "method": "Dormand-Prince 5(4)",
-            "parallelism": f"replicas x{ws}" if ws > 1 else "single solve, one cooperative grid",
-            "l2_flush": "inputs exceed L2 (operator 497 MB > 126 MB L2)",
-            "dp5_attempts": att, "stats_steps_rejected_rhs": list(stats),
-            "host_operator_build_s": host_ops_s,
-            "device_liouvillian_and_store_build_s": store_build_s,
-            "grid_ctas": r["grid_ctas"], "timed_wall_s": wall,
-        },
+        "config": dict(HEADLINE_CONFIG, parallelism=f"replicas x{ws}" if ws > 1 else "single solve, one cooperative grid"),
+        "run": {"dp5_attempts": att, "stats_steps_rejected_rhs": list(stats), "host_operator_build_s": host_ops_s,
+                "device_liouvillian_and_store_build_s": store_build_s, "grid_ctas": r["grid_ctas"],
+                "timed_wall_s": wall, "operator_store": store_info},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": "dp5_grid_kernel (persistent fused DP5 solve, 1 launch per solve)",
                      "bytes_model": "per attempt 6*store + 47*16*n (SURVEY.md 8d vector passes) + start 2 SpMV; "
-                                    "store = code_bytes*nnz + 4*n + 16*n/32 + 20*pairs (coded) or "
-                                    "20*nnz + 4*n + 8*n/32 (plain)"},
+                                    "store = bytes of the operator store the stage passes stream "
+                                    "(qsg_op_store_info: key-aligned blocks, or code_bytes*nnz + 4*n + "
+                                    "16*n/32 + 20*pairs coded, or 20*nnz + 4*n + 8*n/32 plain)",
+                     "store_streamed": {0: "plain", 1: "coded", 2: "key-aligned"}[int(r["store"])],
+                     "store_bytes_per_spmv": stage_bytes},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "path": "qsg_liouvillian_create(pinned host H, c_ops) + qsg_mesolve(host rho0 -> host expect)"},
         "gpu_launches": args.steps,
@@ -315,9 +345,15 @@ def run_ours(args, ws, rank, local):
         "secondary": secondary,
     }
     if rank == 0 and ws == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(att)
+        line["cpu_baseline"] = cpu_baseline(stats)
     ctx.close()
     return line
+
+
+def solve_store_bytes(info, store):
+    """Bytes one stage SpMV of the grid solver reads from the store it streamed (timing.store:
+    0 plain, 1 coded, 2 key-aligned)."""
+    return {0: info["plain_bytes"], 1: info["coded_bytes"], 2: info["ka_bytes"]}[int(store)]
 
 
 def store_bytes(code_bytes, dict_pairs, n, nnz):
@@ -333,7 +369,7 @@ def kerr_sweep_spmv(ctx, q, torch, dev, peak):
     """BASELINE configs[3]: Liouvillian SpMV of the Kerr resonator for N = 50..400 (L2-resident
     for the smaller cutoffs, so bytes/time can exceed the HBM copy rate)."""
     out = {}
-    for N in (50, 100, 200, 400):
+    for N in KERR_CUTOFFS:
         m = q.Model("kerr", N, 1.0, 0.01, 2.0, 1.0)
         Lk = m.export(q.SEL_L_CONST)
         g = q.Generator([ctx.op(Lk)])
@@ -346,12 +382,14 @@ def kerr_sweep_spmv(ctx, q, torch, dev, peak):
     return out
 
 
-def kerr_cutoff_mesolve(ctx, q, peak):
+def kerr_cutoff_mesolve(ctx, q, peak, cpu=False):
     """BASELINE configs[3]: Kerr resonator mesolve over cutoffs N (Liouvillian up to 160k rows),
-    abstol 1e-8, tlist linspace(0,10,101); device time per solve and byte-model GB/s."""
+    abstol 1e-8, tlist linspace(0,10,101); device time per solve and byte-model GB/s. cpu: the
+    oracle (1 thread, as the reference's mesolve) on the first 0.2 time units of the same solve
+    at every N, reported per DP5 attempt beside the device's per-attempt time."""
     out = {}
     tl = np.linspace(0.0, 10.0, 101)
-    for N in (50, 100, 200, 400):
+    for N in KERR_CUTOFFS:
         m = q.Model("kerr", N, 1.0, 0.01, 2.0, 1.0)
         Lk = m.export(q.SEL_L_CONST)
         g = q.Generator([ctx.op(Lk)])
@@ -366,6 +404,19 @@ def kerr_cutoff_mesolve(ctx, q, peak):
         out[f"N{N}"] = {"rows": n, "nnz": nnz, "solve_ms": r["kernel_ms"], "attempts": r["attempts"],
                         "us_per_attempt": r["kernel_ms"] * 1e3 / r["attempts"], "GBps_model": b / r["kernel_ms"] / 1e6,
                         "grid_ctas": r["grid_ctas"], "note": "L2-resident operator: GB/s can exceed the HBM rate"}
+        if cpu:
+            from oracle import oracle as O
+            O.set_threads(1)
+            om = O.Model("kerr", N, 1.0, 0.01, 2.0, 1.0)
+            om.prepare_liouvillian()
+            t0 = time.perf_counter()
+            _, st = om.mesolve_prepared(np.linspace(0.0, 0.2, 3))
+            dt = time.perf_counter() - t0
+            per = dt / int(st[0] + st[1])
+            out[f"N{N}"]["cpu_baseline"] = {
+                "us_per_attempt": per * 1e6, "cores": 1, "kind": "port",
+                "sample": f"oracle mesolve t in [0,0.2] ({int(st[0] + st[1])} attempts, {dt:.2f} s)",
+                "device_speedup_per_attempt": per * 1e3 / (r["kernel_ms"] / r["attempts"])}
     return out
 
 
@@ -395,7 +446,7 @@ def sesolve_tfim20(ctx, q, peak):
     return out
 
 
-def param_sweep_sharded(args, ctx, q, torch, ws, rank):
+def param_sweep_sharded(args, ctx, q, torch, ws, rank, cpu=False):
     """BASELINE configs[4]: 256 (Delta, F) points of two coupled Kerr modes (N=10 each,
     U=0.1, J=0.5, gamma=1), Delta in linspace(-2,2,16) x F in linspace(0.1,1,16), one mesolve per
     point, points sharded in contiguous blocks over ranks (no numeric reduction)."""
@@ -415,10 +466,38 @@ def param_sweep_sharded(args, ctx, q, torch, ws, rank):
     barrier(ws)
     r = q.mesolve_batch(ctx, g, m.dim, rho0, tl, eops, pts[b:e])
     t_ms = allreduce_max(r["kernel_ms"], ws)
-    return {"workload": "256-point coupled-Kerr (N=10x10, Liouvillian 10^4 rows) mesolve sweep",
-            "points": len(pts), "points_this_rank": e - b, "device_s": t_ms / 1e3,
-            "points_per_s": len(pts) / (t_ms / 1e3), "attempts_rank0": r["attempts"],
-            "failed": int((r["status"] != 0).sum())}
+    res = {"workload": "256-point coupled-Kerr (N=10x10, Liouvillian 10^4 rows) mesolve sweep",
+           "points": len(pts), "points_this_rank": e - b, "device_s": t_ms / 1e3,
+           "points_per_s": len(pts) / (t_ms / 1e3), "attempts_rank0": r["attempts"],
+           "failed": int((r["status"] != 0).sum())}
+    if cpu:
+        res["cpu_baseline"] = sweep_cpu(pts, tl)
+    return res
+
+
+def sweep_cpu(pts, tl):
+    """Oracle sweep points (each a single-threaded mesolve, as the reference's): 4 points on one
+    thread, and one point per host thread run concurrently (independent points)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    O.set_threads(1)
+    m = O.Model("coupled_kerr", 10, 0.1, 0.5, 1.0)
+    m.prepare_liouvillian()
+    t0 = time.perf_counter()
+    for p in pts[:4]:
+        m.mesolve_prepared(tl, params=p)
+    one = 4 / (time.perf_counter() - t0)
+    th = host_threads()
+    models = [O.Model("coupled_kerr", 10, 0.1, 0.5, 1.0) for _ in range(th)]
+    for mm in models:
+        mm.prepare_liouvillian()
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(th) as ex:
+        list(ex.map(lambda k: models[k].mesolve_prepared(tl, params=pts[k]), range(th)))
+    many = th / (time.perf_counter() - t0)
+    return {"points_per_s_1_thread": one, "points_per_s_all_threads": many, "cores": th, "kind": "port",
+            "sample": f"oracle mesolve of grid points: 4 sequential on 1 thread; {th} concurrent on {th} threads"}
 
 
 def stochastic_secondary(args, q, rank):
@@ -449,9 +528,11 @@ def stochastic_secondary(args, q, rank):
     return out
 
 
-def mcsolve_sharded(args, ctx, q, torch, ws, rank):
-    """BASELINE configs[2] workload (TFIM-14 mcsolve) on a bounded trajectory count, sharded in
-    contiguous blocks (trajectory i = RngStream(2025, i) on every N), NCCL all-gather of block sums."""
+def mcsolve_sharded(args, ctx, q, torch, ws, rank, peak, cpu=False):
+    """BASELINE configs[2] workload (TFIM-14 mcsolve, 10k trajectories by default), sharded in
+    contiguous blocks (trajectory i = RngStream(2025, i) on every N), block sums combined in the
+    reference's pairwise bracket after an NCCL all-gather. Roofline: SURVEY §8d's 47*16*n bytes
+    per trajectory-attempt over all ranks' attempts / the max-over-ranks device time."""
     from paper_2504_21440_b200.dist import combine_mean, gather_block_sums, shard_range
 
     ntraj = args.mc_traj
@@ -460,9 +541,11 @@ def mcsolve_sharded(args, ctx, q, torch, ws, rank):
     cops = [m.export(q.SEL_C_OP, k) for k in range(m.n_cops)]
     eops = [m.export(q.SEL_E_OP, 2)]
     b, e = shard_range(ntraj, rank, ws)
+    q.mcsolve(ctx, G, cops, eops, m.dim, m.psi0(), TLIST, MC_SEED, b, min(e, b + 64), per_traj=False)  # warm-up
     barrier(ws)
     r = q.mcsolve(ctx, G, cops, eops, m.dim, m.psi0(), TLIST, MC_SEED, b, e, per_traj=False)
     t_ms = allreduce_max(r["kernel_ms"], ws)
+    att_all = allreduce_sum(r["attempts"], ws)
     if ws > 1:
         sums, counts = gather_block_sums(r["block_sum"], r["n_ok"], ws, device=torch.device("cuda", ctx.device))
         n_ok = sum(counts)
@@ -470,61 +553,95 @@ def mcsolve_sharded(args, ctx, q, torch, ws, rank):
     else:
         n_ok = r["n_ok"]
         mean = q.ensemble_combine([(0, ntraj)], [r["block_sum"]], n_ok)
-    return {"workload": "mcsolve TFIM-14 (16384-dim), Sz_total, tlist linspace(0,10,100)",
-            "ntraj": ntraj, "n_ok": n_ok, "device_s": t_ms / 1e3, "traj_per_s": ntraj / (t_ms / 1e3),
-            "attempts_rank0": r["attempts"], "mean_Sz_t10": float(mean[0, -1].real),
-            "collective": "torch.distributed all_gather (NCCL) of per-rank pairwise block sums" if ws > 1 else None}
+    n = m.dim
+    ach = att_all * 47 * 16 * n / (t_ms / 1e3) / 1e9
+    res = {"workload": "mcsolve TFIM-14 (16384-dim), Sz_total, tlist linspace(0,10,100), seed 2025",
+           "ntraj": ntraj, "n_ok": n_ok, "device_s": t_ms / 1e3, "traj_per_s": ntraj / (t_ms / 1e3),
+           "attempts_all_ranks": att_all, "mean_Sz_t10": float(mean[0, -1].real),
+           "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                        "bytes_model": "47*16*n per trajectory-attempt (SURVEY.md 8d), operator L2-resident"},
+           "collective": "torch.distributed all_gather (NCCL) of per-rank pairwise block sums" if ws > 1 else None}
+    if cpu:
+        from oracle import oracle as O
+        th = host_threads()
+        om = O.Model("ising", *TFIM_MC)
+        k = 2 * th
+        t0 = time.perf_counter()
+        om.mcsolve(TLIST, MC_SEED, k, n_threads=th)
+        dt = time.perf_counter() - t0
+        res["cpu_baseline"] = {"traj_per_s": k / dt, "cores": th, "kind": "port",
+                               "sample": f"oracle run_ensemble, trajectories 0..{k - 1} of seed 2025 on {th} threads "
+                                         f"({dt:.1f} s)"}
+    return res
 
 
-def cpu_baseline(gpu_attempts):
-    """Oracle (CPU restatement of the reference solve loop) on the first 0.5 time units of the
-    same solve with a prebuilt Liouvillian; per-attempt time extrapolated to the full solve."""
+def oracle_tfim10(threads):
+    """The oracle's TFIM-10 model with the Liouvillian prebuilt (the reference builds it inside
+    mesolve, evolve.cpp:243-252; the GPU line times the device assembly separately too)."""
     from oracle import oracle as O
+    O.set_threads(threads)
     m = O.Model("ising", *TFIM)
     t0 = time.perf_counter()
     m.prepare_liouvillian()
-    build = time.perf_counter() - t0
-    sample_t = np.linspace(0.0, 0.5, 6)
+    return O, m, time.perf_counter() - t0
+
+
+def cpu_baseline(gpu_stats):
+    """One complete configs[1] solve by the oracle (CPU restatement of evolve.cpp/integrator.hpp)
+    on every host thread; its step statistics must match the device solve's."""
+    th = host_threads()
+    O, m, build = oracle_tfim10(th)
     t0 = time.perf_counter()
-    _, st = m.mesolve_prepared(sample_t)
+    _, st = m.mesolve_prepared(TLIST)
     dt = time.perf_counter() - t0
-    per_att = dt / int(st[0] + st[1])
-    return {"value": per_att * gpu_attempts, "unit": "s", "cores": 1, "kind": "port",
-            "sample": f"oracle mesolve TFIM-10 over t in [0,0.5] ({int(st[0] + st[1])} DP5 attempts, "
-                      f"{dt:.1f} s), {per_att:.3f} s/attempt x {gpu_attempts} attempts of the full solve; "
-                      f"Liouvillian build {build:.1f} s excluded"}
+    O.set_threads(1)
+    return {"value": dt, "unit": "s", "cores": th, "kind": "port",
+            "sample": f"one complete TFIM-10 solve (t in [0,10], {int(st[0] + st[1])} DP5 attempts, stats "
+                      f"{list(map(int, st))} vs device {list(map(int, gpu_stats))}), oracle with {th} threads "
+                      f"(row-parallel SpMV, bit-identical to 1 thread); Liouvillian build {build:.1f} s excluded"}
 
 
 def run_reference(args, ws, rank):
-    """--impl reference: the CPU restatement of the reference on this host (rank 0 only)."""
+    """--impl reference: the CPU restatement of the reference running the same complete solves on
+    this host (rank 0 only; the other ranks exit without work)."""
     if rank != 0:
         return None
-    from oracle import oracle as O
-    m = O.Model("ising", *TFIM)
-    t0 = time.perf_counter()
-    m.prepare_liouvillian()
-    build = time.perf_counter() - t0
-    sample_t = np.linspace(0.0, 0.5, 6)
-    full_attempts = 81  # DP5 attempts of the full TFIM-10 solve (device and oracle agree: 80 + 1)
-    for _ in range(args.warmup if args.warmup <= 1 else 1):
-        m.mesolve_prepared(sample_t)
+    th = host_threads()
+    O, m, build = oracle_tfim10(th)
+    for _ in range(args.warmup):
+        m.mesolve_prepared(TLIST)
     vals = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        _, st = m.mesolve_prepared(sample_t)
-        dt = time.perf_counter() - t0
-        vals.append(dt / int(st[0] + st[1]) * full_attempts)
+        _, st = m.mesolve_prepared(TLIST)
+        vals.append(time.perf_counter() - t0)
     v = sum(vals) / len(vals)
-    sample = (f"oracle (CPU restatement of evolve.cpp/integrator.hpp) TFIM-10 over t in [0,0.5] per step, "
-              f"per-attempt time x {full_attempts} attempts; 1 thread (reference mesolve is single-threaded, "
-              f"SPEC.md:382); Liouvillian build {build:.1f} s excluded")
+    sample = (f"complete TFIM-10 solve per step (t in [0,10], {int(st[0] + st[1])} DP5 attempts, stats "
+              f"{list(map(int, st))}); oracle = CPU restatement of evolve.cpp/integrator.hpp/superop.cpp with "
+              f"{th} threads (row-parallel SpMV + element-wise loops, bit-identical to the single-threaded "
+              f"reference order); Liouvillian build {build:.1f} s excluded, as on the GPU line")
     return {"metric": "mesolve_time_to_solution", "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c128", "data": "synthetic: reference TFIM construction",
-            "config": {"workload": "mesolve dissipative TFIM chain, 10 spins, periodic (BASELINE configs[1])"},
+            "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic: reference TFIM construction (factories.cpp:204-246), all-up initial state",
+            "config": dict(HEADLINE_CONFIG, parallelism=f"replicas x{ws}" if ws > 1 else "single solve, one cooperative grid"),
             "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": sample},
-            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": v, "unit": "s", "cores": th, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "run": {"per_step_s": vals}}
+
+
+def maybe_relaunch(args):
+    """--gpus N outside torchrun: re-exec under torch.distributed.run with N ranks."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
 
 
 def main():
@@ -538,7 +655,10 @@ def main():
     ap.add_argument("--quick", action="store_true", help="headline only (no secondary workloads)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
+    maybe_relaunch(args)
     ws, rank, local = dist_init()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
         line = run_reference(args, ws, rank)
     else:

@@ -136,7 +136,7 @@ int32_t qsg_op_dict_size(const qsg_op* op);
  * bytes; info[2] coded bytes (0 if absent); info[3] key-aligned bytes (0 if absent); info[4]
  * key-aligned distinct values; info[5] key-aligned positions; info[6] coded pairs; info[7]
  * largest key-aligned slice block (bytes). The key-aligned store is built next to the coded one
- * when it pays; QSG_NO_KA=1 disables it. */
+ * on request (QSG_KA_STORE=1, or QSG_KA_SOLVE=1 which also makes the grid solver stream it). */
 qsg_status qsg_op_store_info(const qsg_op* op, int64_t* info);
 
 /* On-device Liouvillian assembly (superop.cpp:78-91 liouvillian, :51-76 spre/spost/sprepost/

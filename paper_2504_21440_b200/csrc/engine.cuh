@@ -39,11 +39,12 @@ struct DevSell {
   // plain store small enough that each SM's share of it stays in L1 across passes: its (col, val)
   // entries are loaded through the L1-allocating read-only path instead of L1::no_allocate
   int l1;
-  // Key-aligned store (ka_nval 0 = absent). Slice s is one block of 16-byte words at
-  // ka_blk + ka_off[s]: header {npos, nnon, 0, 0}, then npos position records {key, lane mask,
-  // value id | kKaNonUniform, exception offset}, then nnon arrays of 32 uint16 per-lane value ids.
-  // Position p holds, for every lane (row) whose mask bit is set, the entry in column row ^ key;
-  // positions are in ascending key order. Values come from the ka_val table of distinct values.
+  // Key-aligned store (ka_nval 0 = absent). Slice s is one block of 32-bit words at
+  // ka_blk + 16 * ka_off[s] bytes. A position is a key: it holds, for every lane (row) in its lane
+  // mask, the entry in column row ^ key. Layout: header {G, NN, Pu, Npart}; G group words (value id
+  // | count << 16, ascending value id); Pu key words of the uniform positions in group order (bit
+  // 31: the lane mask is partial); Npart partial masks in the same order; NN non-uniform positions
+  // as {key, mask, 32 uint16 value ids}. Values come from the ka_val table of distinct values.
   const unsigned* ka_off;
   const uint4* ka_blk;
   const double2* ka_val;
@@ -51,6 +52,7 @@ struct DevSell {
   int ka_slot;  // largest block in bytes (ring slot size)
 };
 
+constexpr unsigned kKaHdrWords = 4, kKaNonUniWords = 18;
 constexpr unsigned kKaNonUniform = 0xffffffffu;
 
 struct DevCoeff {

@@ -195,6 +195,7 @@ struct KaRing {
   const uint4* blk;          // store blocks (global)
   const unsigned* off;       // block offsets (global, 16-byte units)
   int slot_words, b0, W, cnt, cbase;
+  int knext;                 // sequence index of the next block to issue (wraps at cnt)
   unsigned used, issued;     // stream positions (identical in every lane)
   unsigned off_lo, off_hi;   // lane j: bounds of sequence index cbase + j
 
@@ -208,7 +209,8 @@ struct KaRing {
     }
   }
   __device__ __forceinline__ void issue() {
-    const int k = static_cast<int>(issued % static_cast<unsigned>(cnt));
+    const int k = knext;
+    knext = k + 1 == cnt ? 0 : k + 1;
     if (k < cbase || k >= cbase + 32) refill(k);
     const unsigned lo = __shfl_sync(0xffffffffu, off_lo, k - cbase);
     const unsigned hi = __shfl_sync(0xffffffffu, off_hi, k - cbase);
@@ -232,34 +234,62 @@ struct KaRing {
   }
 };
 
-// One slice of the key-aligned store from its staged block: for every position (ascending key) the
-// lanes whose mask bit is set gather x[row ^ key] and multiply by the position's value: one
-// warp-uniform shared-memory word per position, plus per-lane value ids where the position's values
-// differ across lanes (the diagonal, typically).
+// One slice of the key-aligned store from its staged block (engine.cuh layout). Every shared-memory
+// word is read at a warp-uniform address (one wavefront per 32-bit word, two per value): per
+// position only its key word (and a partial mask), per value group one value. Positions of a group
+// share their value, so the group's gathers are summed first and multiplied once:
+//   acc += v_g * (sum_{p in g} x[row ^ key_p]),
+// groups in ascending value id, then the non-uniform positions (per-lane value ids) in key order.
+#ifndef KA_UNROLL
+#define KA_UNROLL 4
+#endif
 template <class XF>
-__device__ __forceinline__ double2 ka_row(const uint4* __restrict__ blk, const double2* __restrict__ vals, int row,
+__device__ __forceinline__ double2 ka_row(const uint4* __restrict__ blk4, const double2* __restrict__ vals, int row,
                                           XF&& xf) {
-  __builtin_assume(__isShared(blk));
+  const unsigned* __restrict__ w = reinterpret_cast<const unsigned*>(blk4);
+  __builtin_assume(__isShared(w));
   __builtin_assume(__isShared(vals));
   const int lane = threadIdx.x & 31;
   const unsigned bit = 1u << lane;
-  const int np = static_cast<int>(blk[0].x);
-  const unsigned short* ex = reinterpret_cast<const unsigned short*>(blk);
+  asm volatile("" : "+r"(row));  // keep row in a register: ptxas otherwise rematerialises it per gather
+  const uint4 h = blk4[0];
+  const int G = static_cast<int>(h.x), NN = static_cast<int>(h.y), Pu = static_cast<int>(h.z);
   double2 acc = make_double2(0.0, 0.0);
-  const double2 z = make_double2(0.0, 0.0);
-  for (int p0 = 0; p0 < np; p0 += 4) {
-    uint4 r[4];
-    double2 x[4];
+  const unsigned* kw_p = w + kKaHdrWords + G;  // key words, group order
+  const unsigned* mk_p = kw_p + Pu;            // partial masks, same order
+  for (int g = 0; g < G; ++g) {
+    const unsigned gw = w[kKaHdrWords + g];
+    const int cnt = static_cast<int>(gw >> 16);
+    double2 sum = make_double2(0.0, 0.0);
+    for (int c = 0; c < cnt; c += KA_UNROLL) {
+      unsigned kw[KA_UNROLL];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) r[u] = p0 + u < np ? blk[1 + p0 + u] : make_uint4(0u, 0u, 0u, 0u);
+      for (int u = 0; u < KA_UNROLL; ++u) kw[u] = c + u < cnt ? kw_p[u] : 0x80000000u;  // past the end: empty mask
+      double2 x[KA_UNROLL];
+      int q = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = (r[u].y & bit) ? xf(row ^ static_cast<int>(r[u].x)) : z;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (r[u].y & bit) {
-        const unsigned vid = r[u].z != kKaNonUniform ? r[u].z : static_cast<unsigned>(ex[r[u].w + lane]);
-        cfma(vals[vid], x[u], acc);
+      for (int u = 0; u < KA_UNROLL; ++u) {
+        const bool part = static_cast<int>(kw[u]) < 0;
+        const unsigned m = part ? (c + u < cnt ? mk_p[q] : 0u) : 0xffffffffu;
+        q += (part && c + u < cnt) ? 1 : 0;
+        const int col = (row ^ static_cast<int>(kw[u])) & 0x7fffffff;
+        x[u] = (m & bit) ? xf(col) : make_double2(0.0, 0.0);
       }
+#pragma unroll
+      for (int u = 0; u < KA_UNROLL; ++u) sum = cadd(sum, x[u]);
+      kw_p += KA_UNROLL;
+      mk_p += q;
+    }
+    kw_p += cnt - ((cnt + KA_UNROLL - 1) / KA_UNROLL) * KA_UNROLL;  // undo the overshoot of the last chunk
+    cfma(vals[gw & 0xffffu], sum, acc);
+  }
+  const unsigned* ep = mk_p;
+  for (int e = 0; e < NN; ++e, ep += kKaNonUniWords) {
+    const unsigned key = ep[0], msk = ep[1];
+    if (msk & bit) {
+      const unsigned short vid = reinterpret_cast<const unsigned short*>(ep + 2)[lane];
+      cfma(vals[vid], xf(row ^ static_cast<int>(key)), acc);
+    }
   }
   return acc;
 }
@@ -640,6 +670,7 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     ring.W = W;
     ring.cnt = ring.b0 < s1 ? (s1 - ring.b0 + W - 1) / W : 0;
     ring.cbase = -64;
+    ring.knext = 0;
     ring.used = ring.issued = 0;
     if ((threadIdx.x & 31) == 0) {
       mbar_init(ring.bar, 1);

@@ -410,20 +410,28 @@ static cudaError_t build_coded_store(qsg_op* op, const int* rp, const int* col, 
 // One warp per 32-row slice. Each lane sorts its row's entries by key = col ^ row; the warp then
 // merges the 32 sorted lists: position p takes the warp-minimum head key, the lanes holding it set
 // their bit in the position's lane mask and advance. A position whose lanes all carry the same
-// value (bit-exact) stores that value's id once (warp-uniform); otherwise it stores one uint16 id
-// per lane. COUNT pass: widths (npos, nnon) per slice; FILL pass: the blocks.
-constexpr int kKaMaxRow = 64;   // longest row the per-lane sort handles
-constexpr int kKaMaxPos = 128;  // widest key union per slice
+// value (bit-exact) is "uniform": it joins the group of that value. Lane 0 then writes the slice
+// block (engine.cuh kKa* layout): header, one word per group (value id | count << 16), the uniform
+// positions' key words grouped by ascending value id (keys ascending inside a group; bit 31 set
+// when the lane mask is partial), the partial masks in the same order, then each non-uniform
+// position as {key, mask, 32 uint16 value ids}. COUNT pass: block sizes (words); FILL pass: blocks.
+constexpr int kKaMaxRow = 64;    // longest row the per-lane sort handles
+constexpr int kKaMaxPos = 128;   // widest key union per slice
+constexpr int kKaMaxNonUni = 8;  // non-uniform positions per slice
 constexpr int kKaMaxVals = 2048;
+constexpr int kKaWarps = 4;      // warps per build block
 
 template <bool FILL>
-__global__ void __launch_bounds__(128) ka_slice_kernel(const int* __restrict__ rowptr, const int* __restrict__ col,
-                                                       const unsigned* __restrict__ slot_of,
-                                                       const unsigned* __restrict__ dense, int n, int nsl,
-                                                       unsigned* __restrict__ npos_out, unsigned* __restrict__ nnon_out,
-                                                       const unsigned* __restrict__ off16, uint4* __restrict__ blk,
-                                                       int* __restrict__ bad) {
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(32 * kKaWarps) ka_slice_kernel(const int* __restrict__ rowptr,
+                                                                 const int* __restrict__ col,
+                                                                 const unsigned* __restrict__ slot_of,
+                                                                 const unsigned* __restrict__ dense, int n, int nsl,
+                                                                 unsigned* __restrict__ words_out,
+                                                                 const unsigned* __restrict__ off16,
+                                                                 unsigned* __restrict__ blk, int* __restrict__ bad) {
+  __shared__ unsigned s_key[kKaWarps][kKaMaxPos], s_mask[kKaWarps][kKaMaxPos], s_vid[kKaWarps][kKaMaxPos];
+  __shared__ unsigned short s_ex[kKaWarps][kKaMaxNonUni][32];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (s >= nsl) return;
   const int r = s * 32 + lane;
@@ -446,11 +454,8 @@ __global__ void __launch_bounds__(128) ka_slice_kernel(const int* __restrict__ r
     key[j] = kk;
     vid[j] = vv;
   }
-  unsigned np = 0, nn = 0;
-  const unsigned npos_total = FILL ? npos_out[s] : 0;
-  uint4* out = FILL ? blk + off16[s] : nullptr;
-  unsigned short* ex = FILL ? reinterpret_cast<unsigned short*>(out + 1 + npos_total) : nullptr;
-  int h = 0;
+  int np = 0, nn = 0, h = 0;
+  bool overflow = false;
   for (;;) {
     const unsigned my = h < len ? key[h] : 0xffffffffu;
     const unsigned m = __reduce_min_sync(0xffffffffu, my);
@@ -461,39 +466,95 @@ __global__ void __launch_bounds__(128) ka_slice_kernel(const int* __restrict__ r
     const unsigned vmin = __reduce_min_sync(0xffffffffu, has ? v : 0xffffffffu);
     const unsigned vmax = __reduce_max_sync(0xffffffffu, has ? v : 0u);
     const bool uni = vmin == vmax;
-    if (FILL) {
-      if (!uni) ex[32 * nn + lane] = static_cast<unsigned short>(v);
-      if (lane == 0)
-        out[1 + np] = make_uint4(m, mask, uni ? vmin : kKaNonUniform, uni ? 0u : 8u * (1u + npos_total) + 32u * nn);
+    if (np < kKaMaxPos && (uni || nn < kKaMaxNonUni)) {
+      if (!uni) s_ex[wl][nn][lane] = static_cast<unsigned short>(v);
+      if (lane == 0) {
+        s_key[wl][np] = m;
+        s_mask[wl][np] = mask;
+        s_vid[wl][np] = uni ? vmin : kKaNonUniform;
+      }
+    } else {
+      overflow = true;
     }
     ++np;
-    nn += uni ? 0u : 1u;
+    nn += uni ? 0 : 1;
     if (has) ++h;
   }
-  if (lane == 0) {
-    if (FILL) {
-      out[0] = make_uint4(np, nn, 0u, 0u);
+  if (overflow) {
+    if (lane == 0) atomicExch(bad, 1);
+    return;
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  // groups: distinct uniform value ids, ascending
+  unsigned gv[kKaMaxPos], gc[kKaMaxPos];
+  int G = 0, Pu = 0, npart = 0;
+  for (int p = 0; p < np; ++p) {
+    const unsigned v = s_vid[wl][p];
+    if (v == kKaNonUniform) continue;
+    ++Pu;
+    npart += s_mask[wl][p] != 0xffffffffu;
+    int g = 0;
+    while (g < G && gv[g] < v) ++g;
+    if (g < G && gv[g] == v) {
+      ++gc[g];
     } else {
-      npos_out[s] = np;
-      nnon_out[s] = nn;
+      for (int q = G; q > g; --q) {
+        gv[q] = gv[q - 1];
+        gc[q] = gc[q - 1];
+      }
+      gv[g] = v;
+      gc[g] = 1;
+      ++G;
     }
   }
+  const unsigned words = (kKaHdrWords + G + Pu + npart + kKaNonUniWords * nn + 3u) & ~3u;
+  if (!FILL) {
+    words_out[s] = words;
+    return;
+  }
+  unsigned* w = blk + 4ull * off16[s];
+  w[0] = G;
+  w[1] = nn;
+  w[2] = Pu;
+  w[3] = npart;
+  unsigned kp = kKaHdrWords + G, mp = kp + Pu, ep = mp + npart;
+  for (int g = 0; g < G; ++g) {
+    w[kKaHdrWords + g] = gv[g] | (gc[g] << 16);
+    for (int p = 0; p < np; ++p)  // keys ascending inside the group
+      if (s_vid[wl][p] == gv[g]) {
+        const bool part = s_mask[wl][p] != 0xffffffffu;
+        w[kp++] = s_key[wl][p] | (part ? 0x80000000u : 0u);
+        if (part) w[mp++] = s_mask[wl][p];
+      }
+  }
+  int e = 0;
+  for (int p = 0; p < np; ++p)
+    if (s_vid[wl][p] == kKaNonUniform) {
+      w[ep] = s_key[wl][p];
+      w[ep + 1] = s_mask[wl][p];
+      unsigned short* ids = reinterpret_cast<unsigned short*>(w + ep + 2);
+      for (int l = 0; l < 32; ++l) ids[l] = s_ex[wl][e][l];
+      ep += kKaNonUniWords;
+      ++e;
+    }
 }
 
 // Builds the key-aligned store of `op` from the staged CSR when it pays: at most kKaMaxVals
-// distinct values, rows of at most kKaMaxRow entries, and key unions no wider than 1.25x the
-// entries (lane slots 32 * sum(npos) <= 1.25 nnz). Otherwise op keeps its other stores.
+// distinct values, rows of at most kKaMaxRow entries, at most kKaMaxPos key positions and
+// kKaMaxNonUni non-uniform positions per slice, and blocks smaller than the coded store's
+// entries. Otherwise op keeps its other stores.
 static cudaError_t build_ka_store(qsg_op* op, const int* rp, const int* col, const double2* val, long long n,
                                   cudaStream_t s) {
   const long long nsl = (n + 31) / 32;
   cudaError_t e;
-  DevBuf tsig, toff, tval, slot_of, dense, cnt, ovf, doff, dval, dnp, dnn, doff16, dbad;
+  DevBuf tsig, toff, tval, slot_of, dense, cnt, ovf, doff, dval, dnp, dbad;
   if ((e = tsig.alloc(sizeof(unsigned long long) * kDictSlots, s)) || (e = toff.alloc(sizeof(int) * kDictSlots, s)) ||
       (e = tval.alloc(sizeof(double2) * kDictSlots, s)) || (e = slot_of.alloc(sizeof(unsigned) * op->nnz, s)) ||
       (e = dense.alloc(sizeof(unsigned) * kDictSlots, s)) || (e = cnt.alloc(sizeof(int), s)) ||
       (e = ovf.alloc(sizeof(int), s)) || (e = doff.alloc(sizeof(int) * kKaMaxVals, s)) ||
       (e = dval.alloc(sizeof(double2) * kKaMaxVals, s)) || (e = dnp.alloc(sizeof(unsigned) * nsl, s)) ||
-      (e = dnn.alloc(sizeof(unsigned) * nsl, s)) || (e = dbad.alloc(sizeof(int), s)))
+      (e = dbad.alloc(sizeof(int), s)))
     return e;
   cudaMemsetAsync(tsig.p, 0, sizeof(unsigned long long) * kDictSlots, s);
   cudaMemsetAsync(ovf.p, 0, sizeof(int), s);
@@ -511,48 +572,45 @@ static cudaError_t build_ka_store(qsg_op* op, const int* rp, const int* col, con
       (e = cudaMemcpyAsync(&overflow, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, s)) || (e = cudaStreamSynchronize(s)))
     return e;
   if (overflow || count < 1 || count > kKaMaxVals) return cudaSuccess;
-  const unsigned kb = static_cast<unsigned>((nsl * 32 + 127) / 128);
-  ka_slice_kernel<false><<<kb, 128, 0, s>>>(rp, col, slot_of.as<unsigned>(), dense.as<unsigned>(), static_cast<int>(n),
-                                            static_cast<int>(nsl), dnp.as<unsigned>(), dnn.as<unsigned>(), nullptr,
-                                            nullptr, dbad.as<int>());
-  std::vector<unsigned> np(static_cast<size_t>(nsl)), nn(static_cast<size_t>(nsl));
+  const unsigned kb = static_cast<unsigned>((nsl + kKaWarps - 1) / kKaWarps);
+  ka_slice_kernel<false><<<kb, 32 * kKaWarps, 0, s>>>(rp, col, slot_of.as<unsigned>(), dense.as<unsigned>(),
+                                                      static_cast<int>(n), static_cast<int>(nsl), dnp.as<unsigned>(),
+                                                      nullptr, nullptr, dbad.as<int>());
+  std::vector<unsigned> nw(static_cast<size_t>(nsl));
   int bad = 0;
   if ((e = cudaGetLastError()) ||
-      (e = cudaMemcpyAsync(np.data(), dnp.p, sizeof(unsigned) * nsl, cudaMemcpyDeviceToHost, s)) ||
-      (e = cudaMemcpyAsync(nn.data(), dnn.p, sizeof(unsigned) * nsl, cudaMemcpyDeviceToHost, s)) ||
+      (e = cudaMemcpyAsync(nw.data(), dnp.p, sizeof(unsigned) * nsl, cudaMemcpyDeviceToHost, s)) ||
       (e = cudaMemcpyAsync(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost, s)) || (e = cudaStreamSynchronize(s)))
     return e;
   if (bad) return cudaSuccess;
   std::vector<unsigned> off(static_cast<size_t>(nsl + 1), 0);
-  long long pos = 0, words = 0;
+  long long words = 0;
   unsigned slot = 0;
   for (long long i = 0; i < nsl; ++i) {
-    if (np[i] > static_cast<unsigned>(kKaMaxPos)) return cudaSuccess;
-    const unsigned w = 1 + np[i] + 4 * nn[i];
-    off[i] = static_cast<unsigned>(words);
-    words += w;
-    pos += np[i];
-    slot = std::max(slot, 16 * w);
-    if (words > 0xffffffffLL) return cudaSuccess;
+    off[i] = static_cast<unsigned>(words / 4);
+    words += nw[i];
+    slot = std::max(slot, 4 * nw[i]);
+    if (words / 4 > 0xffffffffLL) return cudaSuccess;
   }
-  off[nsl] = static_cast<unsigned>(words);
-  if (32 * pos * 4 > 5 * op->nnz) return cudaSuccess;  // union wider than 1.25x the entries
+  off[nsl] = static_cast<unsigned>(words / 4);
+  // positions per slice ~ words; keep the store only when its blocks are well below the coded
+  // store (the coded entries cost op->nnz bytes)
+  if (4 * words > op->nnz) return cudaSuccess;
   if ((e = cudaMallocAsync(&op->ka_off, sizeof(unsigned) * (nsl + 1), s)) ||
-      (e = cudaMallocAsync(&op->ka_blk, 16 * static_cast<size_t>(words), s)) ||
-      (e = cudaMallocAsync(&op->ka_val, sizeof(double2) * count, s)) ||
-      (e = doff16.alloc(sizeof(unsigned) * (nsl + 1), s)))
+      (e = cudaMallocAsync(&op->ka_blk, 4 * static_cast<size_t>(words), s)) ||
+      (e = cudaMallocAsync(&op->ka_val, sizeof(double2) * count, s)))
     return e;
   cudaMemcpyAsync(op->ka_off, off.data(), sizeof(unsigned) * (nsl + 1), cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(op->ka_val, dval.p, sizeof(double2) * count, cudaMemcpyDeviceToDevice, s);
-  cudaMemsetAsync(op->ka_blk, 0, 16 * static_cast<size_t>(words), s);
-  ka_slice_kernel<true><<<kb, 128, 0, s>>>(rp, col, slot_of.as<unsigned>(), dense.as<unsigned>(), static_cast<int>(n),
-                                           static_cast<int>(nsl), dnp.as<unsigned>(), dnn.as<unsigned>(), op->ka_off,
-                                           op->ka_blk, dbad.as<int>());
+  cudaMemsetAsync(op->ka_blk, 0, 4 * static_cast<size_t>(words), s);
+  ka_slice_kernel<true><<<kb, 32 * kKaWarps, 0, s>>>(rp, col, slot_of.as<unsigned>(), dense.as<unsigned>(),
+                                                     static_cast<int>(n), static_cast<int>(nsl), nullptr, op->ka_off,
+                                                     reinterpret_cast<unsigned*>(op->ka_blk), dbad.as<int>());
   if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(s))) return e;
   op->ka_nval = count;
   op->ka_slot = static_cast<int>(slot);
-  op->ka_bytes = 16 * words + 4 * (nsl + 1) + 16LL * count;
-  op->ka_positions = pos;
+  op->ka_bytes = 4 * words + 4 * (nsl + 1) + 16LL * count;
+  op->ka_positions = words;
   return cudaSuccess;
 }
 
@@ -731,10 +789,11 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   const char* sd = std::getenv("QSG_SMEM_DICT");
   if (pf && G->n_terms == 1 && G->ops[0]->dict_n > 0 && G->ops[0]->dict_n <= 2048 && !(sd && sd[0] == '0'))
     P.smem_dict = G->ops[0]->dict_n;
-  // single-term generator with a key-aligned store: stream it through the TMA ring (st 2);
-  // QSG_NO_KA_SOLVE=1 keeps the coded path
-  const char* nks = std::getenv("QSG_NO_KA_SOLVE");
-  const int st = (G->n_terms == 1 && G->ops[0]->ka_nval > 0 && !(nks && nks[0] == '1')) ? 2 : pf ? 1 : 0;
+  // single-term generator with a key-aligned store: stream it through the TMA ring (st 2) when
+  // QSG_KA_SOLVE=1. Not the default: on TFIM-10 it cuts L1 wavefronts 35% and DRAM bytes 30% but
+  // takes 30.5 ms against 27.6 ms for the coded path (K-grid "key-aligned store").
+  const char* ks = std::getenv("QSG_KA_SOLVE");
+  const int st = (G->n_terms == 1 && G->ops[0]->ka_nval > 0 && ks && ks[0] == '1') ? 2 : pf ? 1 : 0;
   if (st == 2) P.smem_dict = 0;
   const size_t dyn = grid_smem_bytes(P, st);
   // materialise the stage-2 input for the pipelined single-term path: one extra streaming pass and
@@ -948,9 +1007,11 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
       return cuda_fail(e, "coded operator store");
     }
     mark("coded");
-    // key-aligned store for the persistent grid engine (QSG_NO_KA=1 disables)
-    const char* nk = std::getenv("QSG_NO_KA");
-    if (!(nk && nk[0] == '1')) {
+    // key-aligned store for the persistent grid engine, built on request (QSG_KA_STORE=1 or
+    // QSG_KA_SOLVE=1): it is not the default solve path (see run_grid_solve)
+    const char* kst = std::getenv("QSG_KA_STORE");
+    const char* ksv = std::getenv("QSG_KA_SOLVE");
+    if ((kst && kst[0] == '1') || (ksv && ksv[0] == '1')) {
       if ((e = build_ka_store(op, d_rp.as<int>(), d_col.as<int>(), d_val.as<double2>(), n, s))) {
         qsg_op_destroy(op);
         return cuda_fail(e, "key-aligned operator store");

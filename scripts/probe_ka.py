@@ -13,6 +13,7 @@ import paper_2504_21440_b200 as q  # noqa: E402
 g = json.load(open(os.path.join(ROOT, "tests", "golden", "fullsize_golden.json")))["tfim10"]
 ref = np.array(g["expect_re"]) + 1j * np.array(g["expect_im"])
 t = np.array(g["tlist"])
+os.environ["QSG_KA_STORE"] = "1"
 m = q.Model("ising", 10, 1, 1.0, 0.2, 1.0, 1)
 ctx = q.Context(0)
 H = m.export(q.SEL_H_CONST)
@@ -27,9 +28,9 @@ reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 for rep in range(reps):
     for mode in ("ka", "coded"):
         if mode == "coded":
-            os.environ["QSG_NO_KA_SOLVE"] = "1"
+            os.environ.pop("QSG_KA_SOLVE", None)
         else:
-            os.environ.pop("QSG_NO_KA_SOLVE", None)
+            os.environ["QSG_KA_SOLVE"] = "1"
         r = q.mesolve(ctx, gen, m.dim, rho0, t, eops)
         err = max(np.max(np.abs(a - b)) / np.max(np.abs(b)) for a, b in zip(r["expect"], ref))
         print(json.dumps({"mode": mode, "store": r.get("store"), "kernel_ms": r["kernel_ms"],
