@@ -533,34 +533,40 @@ def mcsolve_sharded(args, ctx, q, torch, ws, rank, peak, cpu=False):
     contiguous blocks (trajectory i = RngStream(2025, i) on every N), block sums combined in the
     reference's pairwise bracket after an NCCL all-gather. Roofline: SURVEY §8d's 47*16*n bytes
     per trajectory-attempt over all ranks' attempts / the max-over-ranks device time."""
-    from paper_2504_21440_b200.dist import combine_mean, gather_block_sums, shard_range
+    from paper_2504_21440_b200.dist import ProductComm, combine_leaves, ensemble_shards, gather_leaf_sums
 
     ntraj = args.mc_traj
     m = q.Model("ising", *TFIM_MC)
     G = q.Generator([ctx.op(m.export(q.SEL_MC_GEN))])
     cops = [m.export(q.SEL_C_OP, k) for k in range(m.n_cops)]
     eops = [m.export(q.SEL_E_OP, 2)]
-    b, e = shard_range(ntraj, rank, ws)
+    shards = ensemble_shards(ntraj, ws)
+    b, e, leaves = shards[rank]
+    rel = [(lo - b, hi - b) for lo, hi in leaves]  # leaf positions in this rank's completed list
     q.mcsolve(ctx, G, cops, eops, m.dim, m.psi0(), TLIST, MC_SEED, b, min(e, b + 64), per_traj=False)  # warm-up
+    comm = ProductComm(ctx, rank, ws) if ws > 1 else None
     barrier(ws)
-    r = q.mcsolve(ctx, G, cops, eops, m.dim, m.psi0(), TLIST, MC_SEED, b, e, per_traj=False)
+    r = q.mcsolve(ctx, G, cops, eops, m.dim, m.psi0(), TLIST, MC_SEED, b, e, per_traj=False, ranges=rel)
     t_ms = allreduce_max(r["kernel_ms"], ws)
     att_all = allreduce_sum(r["attempts"], ws)
     if ws > 1:
-        sums, counts = gather_block_sums(r["block_sum"], r["n_ok"], ws, device=torch.device("cuda", ctx.device))
-        n_ok = sum(counts)
-        mean = combine_mean(ntraj, ws, sums, counts)
+        nl = max(len(s[2]) for s in shards)
+        sums, counts = gather_leaf_sums(r["range_sums"], r["n_ok"], nl, ws, comm=comm)
+        comm.close()
     else:
-        n_ok = r["n_ok"]
-        mean = q.ensemble_combine([(0, ntraj)], [r["block_sum"]], n_ok)
+        sums, counts = [r["range_sums"]], [r["n_ok"]]
+    n_ok = sum(counts)
+    mean = combine_leaves(ntraj, ws, sums, counts) if n_ok == ntraj else None
     n = m.dim
     ach = att_all * 47 * 16 * n / (t_ms / 1e3) / 1e9
     res = {"workload": "mcsolve TFIM-14 (16384-dim), Sz_total, tlist linspace(0,10,100), seed 2025",
            "ntraj": ntraj, "n_ok": n_ok, "device_s": t_ms / 1e3, "traj_per_s": ntraj / (t_ms / 1e3),
-           "attempts_all_ranks": att_all, "mean_Sz_t10": float(mean[0, -1].real),
+           "attempts_all_ranks": att_all, "mean_Sz_t10": None if mean is None else float(mean[0, -1].real),
            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                         "bytes_model": "47*16*n per trajectory-attempt (SURVEY.md 8d), operator L2-resident"},
-           "collective": "torch.distributed all_gather (NCCL) of per-rank pairwise block sums" if ws > 1 else None}
+           "shards": "whole pairwise-bracket subtrees per rank (dist.ensemble_shards), sums on the device",
+           "collective": "product NCCL all-gather (qsg_comm_allgather) of per-rank bracket-subtree sums"
+                         if ws > 1 else None}
     if cpu:
         from oracle import oracle as O
         th = host_threads()

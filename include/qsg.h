@@ -218,11 +218,22 @@ typedef struct {
   double* jump_time;         /* n_blk x jump_capacity                                */
   int32_t* jump_channel;     /* n_blk x jump_capacity                                */
   int64_t jump_capacity;
+  /* optional: pairwise_sum of each of n_ranges sub-ranges [range_lo[r], range_hi[r]) of the
+   * block's completed-trajectory list (positions in that list, ascending), computed on the device;
+   * range_sums: n_ranges x (n_e x n_t) complex. A rank whose trajectories are several subtrees of
+   * the global bracket returns one sum per subtree (paper_2504_21440_b200/dist.py). */
+  int32_t n_ranges;
+  const int64_t* range_lo;
+  const int64_t* range_hi;
+  double* range_sums;
 } qsg_mc_out;
 
 /* Runs trajectories traj_begin..traj_end-1; trajectory i draws from RngStream(seed, i)
  * (trajectories.cpp:42), so any partition of the index range gives identical per-trajectory
- * results. G = -i*H_eff generator (trajectories.cpp:229-237), c_ops / e_ops as CSR. */
+ * results. G = -i*H_eff generator (trajectories.cpp:229-237), c_ops / e_ops as CSR. The ensemble
+ * sums are accumulated on the device (the pairwise bracket of trajectories.cpp:17-22 over the
+ * completed trajectories, bit-identical to the host recursion); per-trajectory expectations are
+ * copied back only when per_traj_expect is non-NULL. */
 qsg_status qsg_mcsolve(qsg_ctx* ctx, const qsg_generator* G, int32_t n_c, const qsg_csr* c_ops,
                        int32_t n_e, const qsg_csr* e_ops, int64_t d, const double* psi0,
                        const double* tlist, int64_t n_t, const double* params, int32_t n_params,
@@ -235,6 +246,24 @@ qsg_status qsg_mcsolve(qsg_ctx* ctx, const qsg_generator* G, int32_t n_c, const 
 qsg_status qsg_ensemble_combine(int32_t n_blocks, const int64_t* block_begin,
                                 const int64_t* block_end, const double* block_sums,
                                 int64_t n_vals, int64_t n_ok_total, double* mean);
+
+/* ---- NCCL communicators: the one exchange step of sharded ensembles ----------
+ * Replaces run_ensemble's in-process combine (trajectories.cpp:31-58,82-83) when trajectories are
+ * spread over GPUs. qsg_comm_init_rank: one rank per process (ncclCommInitRank; rank 0 makes the
+ * id with qsg_comm_unique_id and the caller broadcasts it); qsg_comm_init_all: every device of
+ * one process (ncclCommInitAll; each comm gets its own context, distinct devices only).
+ * qsg_comm_allgather: recv[r*count ..] = rank r's `count` doubles (host or device buffers),
+ * synchronous on the comm's context stream. NCCL is loaded at run time (the process's own copy
+ * if one is already loaded); without it these return QSG_NCCL_ERROR. */
+typedef struct qsg_comm qsg_comm;
+int32_t qsg_nccl_version(void);
+qsg_status qsg_comm_unique_id(uint8_t* id128);
+qsg_status qsg_comm_init_rank(qsg_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t* id128,
+                              qsg_comm** out);
+qsg_status qsg_comm_init_all(int32_t n_dev, const int32_t* devices, qsg_comm** out);
+qsg_ctx* qsg_comm_ctx(qsg_comm* comm);
+void qsg_comm_destroy(qsg_comm* comm);
+qsg_status qsg_comm_allgather(qsg_comm* comm, const double* send, int64_t count, double* recv);
 
 /* ---- parameter sweeps (a14: one mesolve per parameter point) ---------------------------- */
 /* n_points independent mesolve runs of the same td Liouvillian with per-point params

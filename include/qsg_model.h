@@ -58,12 +58,14 @@ qsg_status qsg_model_sesolve(qsg_model* m, int32_t device, const double* tlist, 
                              double* expect, int64_t* stats, double* device_ms);
 /* mean: n_e x n_t; per_traj (optional): ntraj x n_e x n_t; traj_stats: ensemble totals
  * (steps, rejected, rhs_evals over completed trajectories); jump arrays
- * ntraj x jump_cap. n_devices/devices shard trajectories over several GPUs in-process. */
+ * ntraj x jump_cap. n_devices/devices shard trajectories over several GPUs in-process (NCCL
+ * all-gather of bracket-subtree sums between distinct devices). stddev (optional): n_e x n_t
+ * sample standard deviation of Re over the trajectories (ensemble_stddev, trajectories.cpp:94-104). */
 qsg_status qsg_model_mcsolve(qsg_model* m, int32_t n_devices, const int32_t* devices, const double* tlist,
                              int64_t n_t, const double* params, int32_t n_params, uint64_t seed,
                              int32_t ntraj, const qsg_solve_opts* opts, double* mean, double* per_traj,
                              int64_t* traj_stats, int32_t* n_jumps, double* jump_time, int32_t* jump_channel,
-                             int32_t jump_cap, int32_t* n_failed, double* device_ms);
+                             int32_t jump_cap, int32_t* n_failed, double* device_ms, double* stddev);
 /* qsim::ssesolve (every model c_op is a measurement channel, as the reference scenario's
  * "ssesolve" jc assembly) / qsim::smesolve (model c_ops[0:n_det) unmonitored, the rest measured).
  * mean: n_e x n_t; per_traj (optional): ntraj x n_e x n_t; w_* (optional, store_measurement):

@@ -150,6 +150,15 @@ struct TrajectoryEnsembleResult {
 
 std::vector<double> ensemble_stddev(const TrajectoryEnsembleResult& result);  // n_e x n_t col-major
 
+// Sharding of trajectories [0, ntraj) over nshards devices or ranks: each shard is a contiguous
+// run of whole subtrees ("leaves") of run_ensemble's pairwise bracket (trajectories.cpp:17-22), so
+// per-leaf sums combine into the single-device mean bit for bit (qsg_ensemble_combine).
+struct EnsembleShard {
+  long begin = 0, end = 0;
+  std::vector<std::pair<long, long>> leaves;
+};
+std::vector<EnsembleShard> ensemble_shards(long ntraj, int nshards);
+
 TrajectoryEnsembleResult mcsolve(const TimeDependentOperator& h, const QuantumObject& psi0,
                                  std::span<const double> tlist, std::span<const QuantumObject> c_ops,
                                  std::span<const QuantumObject> e_ops, const EnsembleOptions& ens = {},

@@ -76,7 +76,8 @@ class _Timing(C.Structure):
 class _McOut(C.Structure):
     _fields_ = [("per_traj_expect", DP), ("block_sum", DP), ("n_ok", I64P), ("failed", I32P),
                 ("fail_time", DP), ("traj_stats", I64P), ("jump_count", I32P),
-                ("jump_time", DP), ("jump_channel", I32P), ("jump_capacity", C.c_int64)]
+                ("jump_time", DP), ("jump_channel", I32P), ("jump_capacity", C.c_int64),
+                ("n_ranges", C.c_int32), ("range_lo", I64P), ("range_hi", I64P), ("range_sums", DP)]
 
 
 class _SdeOut(C.Structure):
@@ -360,8 +361,10 @@ def generator_apply_timed(ctx: Context, gen: Generator, y_dev, out_dev, reps=20,
 
 def mcsolve(ctx: Context, G: Generator, c_ops, e_ops, d: int, psi0, tlist, seed: int, traj_begin: int,
             traj_end: int, params=None, abstol=1e-8, reltol=1e-6, max_steps=10_000_000, jump_cap=256,
-            per_traj=True):
-    """qsg_mcsolve: trajectories traj_begin..traj_end-1 of the ensemble (RngStream(seed, i))."""
+            per_traj=True, ranges=None):
+    """qsg_mcsolve: trajectories traj_begin..traj_end-1 of the ensemble (RngStream(seed, i)).
+    ranges: optional [(lo, hi), ...] positions in the block's completed-trajectory list whose
+    pairwise sums are returned as "range_sums" (n_ranges x n_e x n_t)."""
     t = np.ascontiguousarray(tlist, np.float64)
     prm = None if params is None else np.ascontiguousarray(params, np.float64)
     o, _ = _opts(abstol, reltol, max_steps, False, None)
@@ -375,9 +378,13 @@ def mcsolve(ctx: Context, G: Generator, c_ops, e_ops, d: int, psi0, tlist, seed:
     jcount = np.zeros(nb, np.int32)
     jt = np.zeros(nb * jump_cap)
     jc = np.zeros(nb * jump_cap, np.int32)
+    nr = 0 if not ranges else len(ranges)
+    rlo = np.ascontiguousarray([r[0] for r in ranges] if nr else [0], np.int64)
+    rhi = np.ascontiguousarray([r[1] for r in ranges] if nr else [0], np.int64)
+    rs = np.zeros(max(1, nr * ne * nt), np.complex128)
     out = _McOut(_dp(per), _dp(bsum), C.pointer(nok), failed.ctypes.data_as(I32P), _dp(ftime),
                  tst.ctypes.data_as(I64P), jcount.ctypes.data_as(I32P), _dp(jt), jc.ctypes.data_as(I32P),
-                 jump_cap)
+                 jump_cap, nr, rlo.ctypes.data_as(I64P), rhi.ctypes.data_as(I64P), _dp(rs))
     tm = _Timing()
     y0 = np.ascontiguousarray(psi0, np.complex128)
     _check(lib().qsg_mcsolve(ctx._h, C.byref(G._g), len(c_ops), _csr_array(c_ops), ne, _csr_array(e_ops), d,
@@ -388,6 +395,7 @@ def mcsolve(ctx: Context, G: Generator, c_ops, e_ops, d: int, psi0, tlist, seed:
     return {
         "per_traj": None if per is None else per.reshape(nb, nt, ne).transpose(0, 2, 1).copy(),
         "block_sum": bsum[: ne * nt].reshape(nt, ne).T.copy(),
+        "range_sums": [rs[k * ne * nt:(k + 1) * ne * nt].reshape(nt, ne).T.copy() for k in range(nr)],
         "n_ok": nok.value,
         "failed": failed,
         "stats": tst.reshape(nb, 3),
@@ -509,7 +517,7 @@ def _bind_model_api(L):
     L.qsg_model_smesolve.argtypes = [P, C.c_int32, C.c_int32, DP, C.c_int64, DP, C.c_int32, C.c_uint64,
                                      C.c_int32, C.c_double, C.c_int32, DP, DP, DP, DP, DP, I64P, DP, DP]
     L.qsg_model_mcsolve.argtypes = [P, C.c_int32, I32P, DP, C.c_int64, DP, C.c_int32, C.c_uint64, C.c_int32,
-                                    C.POINTER(_Opts), DP, DP, I64P, I32P, DP, I32P, C.c_int32, I32P, DP]
+                                    C.POINTER(_Opts), DP, DP, I64P, I32P, DP, I32P, C.c_int32, I32P, DP, DP]
 
 
 # export selectors of qsg_model_export (include/qsg_model.h)
@@ -629,16 +637,17 @@ class Model:
         jc = np.zeros(ntraj * jump_cap, np.int32)
         nf = C.c_int32(0)
         ms = C.c_double(0)
+        sd = np.zeros(ne * nt)
         dv = np.ascontiguousarray(devices, np.int32)
         _check(lib().qsg_model_mcsolve(self._h, len(dv), dv.ctypes.data_as(I32P), _dp(t), nt, _dp(prm), len(prm),
                                        seed, ntraj, C.byref(o), _dp(mean), _dp(per), st.ctypes.data_as(I64P),
                                        nj.ctypes.data_as(I32P), _dp(jt), jc.ctypes.data_as(I32P), jump_cap,
-                                       C.byref(nf), C.byref(ms)))
+                                       C.byref(nf), C.byref(ms), _dp(sd)))
         jumps = [list(zip(jt[i * jump_cap:i * jump_cap + min(nj[i], jump_cap)].tolist(),
                           jc[i * jump_cap:i * jump_cap + min(nj[i], jump_cap)].tolist())) for i in range(ntraj)]
         return {"mean": mean.reshape(nt, ne).T.copy(), "per_traj": per.reshape(ntraj, nt, ne).transpose(0, 2, 1).copy(),
                 "stats": tuple(int(x) for x in st), "njumps": nj, "jumps": jumps, "failed": nf.value,
-                "kernel_ms": ms.value}
+                "kernel_ms": ms.value, "stddev": sd.reshape(nt, ne).T.copy()}
 
 
 def op_storage(op: "Operator"):

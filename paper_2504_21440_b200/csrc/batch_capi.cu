@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "batch_engine.h"
+#include "ensemble.h"
 #include "qsg_internal.h"
 
 using namespace qsg;
@@ -37,21 +38,20 @@ qsg_status make_sell(qsg_ctx* ctx, const qsg_csr& a, TmpOps& keep, DevSell& out)
   return QSG_OK;
 }
 
-// pairwise_sum over [lo, hi) of the completed trajectories' matrices (trajectories.cpp:17-22)
-void pairwise(const std::vector<const double*>& m, size_t lo, size_t hi, size_t nv, double* out) {
-  if (hi - lo == 1) {
-    std::copy(m[lo], m[lo] + 2 * nv, out);
-    return;
-  }
-  const size_t mid = lo + (hi - lo) / 2;
-  std::vector<double> r(2 * nv);
-  pairwise(m, lo, mid, nv, out);
-  pairwise(m, mid, hi, nv, r.data());
-  for (size_t i = 0; i < 2 * nv; ++i) out[i] += r[i];
-}
+// Device-side ensemble sums requested from run_batch (mcsolve): n_ranges == 0 = one sum over
+// every completed trajectory of the block.
+struct SumReq {
+  bool on = false;
+  long long nv = 0;
+  int n_ranges = 0;
+  const long long* lo = nullptr;
+  const long long* hi = nullptr;
+};
 
 struct RunOut {
   std::vector<double2> expect;
+  std::vector<double2> sums;  // SumReq results, n_ranges (or 1) x nv
+  long long n_ok = 0;
   std::vector<int> status, jcount, jch;
   std::vector<double> ftime, jtime;
   std::vector<long long> stats;
@@ -63,7 +63,8 @@ struct RunOut {
 };
 
 // Runs systems [sys_begin, sys_begin + n_sys) through the batch kernel and downloads outputs.
-qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap, RunOut& o) {
+qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap, RunOut& o,
+                     bool want_expect = true, const SumReq& req = SumReq{}) {
   cudaStream_t s = ctx->stream;
   cudaError_t ce;
   P.n_systems = n_sys;
@@ -176,14 +177,20 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   cudaEventRecord(ctx->ev[2], s);
   if ((ce = launch_batch(P, layout, grid, cs, s))) return cuda_fail(ce, "batch launch");
   cudaEventRecord(ctx->ev[3], s);
-  o.expect.resize(nvals * n_sys);
+  if (req.on && req.nv > 0) {  // ensemble bracket sums on the device (K7)
+    if ((ce = device_bracket_sums(ex.as<double2>(), st.as<int>(), n_sys, static_cast<long long>(nvals), req.n_ranges,
+                                  req.lo, req.hi, s, o.n_ok, o.sums)))
+      return cuda_fail(ce, "ensemble sums");
+  }
+  o.expect.resize(want_expect ? nvals * n_sys : 0);
   o.status.resize(n_sys);
   o.ftime.resize(n_sys);
   o.stats.resize(3 * n_sys);
   o.jcount.resize(n_sys);
   o.jtime.resize(std::max<long long>(1, n_sys * jump_cap));
   o.jch.resize(std::max<long long>(1, n_sys * jump_cap));
-  if ((ce = cudaMemcpyAsync(o.expect.data(), ex.p, nvals * n_sys * sizeof(double2), cudaMemcpyDeviceToHost, s)) ||
+  if ((want_expect &&
+       (ce = cudaMemcpyAsync(o.expect.data(), ex.p, nvals * n_sys * sizeof(double2), cudaMemcpyDeviceToHost, s))) ||
       (ce = cudaMemcpyAsync(o.status.data(), st.p, sizeof(int) * n_sys, cudaMemcpyDeviceToHost, s)) ||
       (ce = cudaMemcpyAsync(o.ftime.data(), ft.p, sizeof(double) * n_sys, cudaMemcpyDeviceToHost, s)) ||
       (ce = cudaMemcpyAsync(o.stats.data(), stt.p, sizeof(long long) * 3 * n_sys, cudaMemcpyDeviceToHost, s)) ||
@@ -277,11 +284,25 @@ extern "C" qsg_status qsg_mcsolve(qsg_ctx* ctx, const qsg_generator* G, int32_t 
   P.n_params = n_params;
   const long long nsys = traj_end - traj_begin;
   const int cap = static_cast<int>(std::max<int64_t>(1, out ? out->jump_capacity : 1));
-  RunOut o;
-  if (qsg_status st = run_batch(ctx, P, nsys, std::max(cap, 64), o)) return st;
-  const int run_cap = std::max(cap, 64);
   const size_t nv = static_cast<size_t>(n_e) * n_t;
-  std::vector<const double*> okm;
+  RunOut o;
+  SumReq req;
+  std::vector<long long> rlo, rhi;
+  req.on = nv > 0;
+  req.nv = static_cast<long long>(nv);
+  if (out && out->n_ranges > 0) {  // the caller's sub-ranges, then the whole list for block_sum
+    rlo.assign(out->range_lo, out->range_lo + out->n_ranges);
+    rhi.assign(out->range_hi, out->range_hi + out->n_ranges);
+    rlo.push_back(0);
+    rhi.push_back(-1);
+    req.n_ranges = out->n_ranges + 1;
+    req.lo = rlo.data();
+    req.hi = rhi.data();
+  }
+  const bool want_expect = out && out->per_traj_expect;
+  if (qsg_status st = run_batch(ctx, P, nsys, std::max(cap, 64), o, want_expect, req)) return st;
+  const int run_cap = std::max(cap, 64);
+  long long n_ok = 0;
   for (long long i = 0; i < nsys; ++i) {
     const bool ok = o.status[i] == kDone;
     if (out) {
@@ -299,16 +320,18 @@ extern "C" qsg_status qsg_mcsolve(qsg_ctx* ctx, const qsg_generator* G, int32_t 
         if (out->jump_time) out->jump_time[i * cap + j] = jt[j];
         if (out->jump_channel) out->jump_channel[i * cap + j] = jc[j];
       }
-      if (out->per_traj_expect)
+      if (want_expect && nv > 0)
         std::copy(reinterpret_cast<const double*>(o.expect.data() + i * nv),
                   reinterpret_cast<const double*>(o.expect.data() + (i + 1) * nv), out->per_traj_expect + 2 * i * nv);
     }
-    if (ok) okm.push_back(reinterpret_cast<const double*>(o.expect.data() + i * nv));
+    n_ok += ok ? 1 : 0;
   }
-  if (out && out->n_ok) *out->n_ok = static_cast<int64_t>(okm.size());
-  if (out && out->block_sum) {
-    if (okm.empty()) std::fill(out->block_sum, out->block_sum + 2 * nv, 0.0);
-    else pairwise(okm, 0, okm.size(), nv, out->block_sum);
+  if (out && out->n_ok) *out->n_ok = n_ok;
+  if (out && nv > 0) {  // sums from the device bracket (zeros when nothing completed)
+    const double* sums = reinterpret_cast<const double*>(o.sums.data());
+    const int nr = out->n_ranges > 0 ? out->n_ranges : 0;
+    if (nr > 0 && out->range_sums) std::copy(sums, sums + 2 * nv * nr, out->range_sums);
+    if (out->block_sum) std::copy(sums + 2 * nv * nr, sums + 2 * nv * (nr + 1), out->block_sum);
   }
   if (timing) {
     timing->kernel_ms = o.kernel_ms;

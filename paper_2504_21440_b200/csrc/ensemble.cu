@@ -1,10 +1,91 @@
-// Ensemble combine (trajectories.cpp:17-22, 82-83) — placeholder entry points filled in by the
-// batched trajectory engine (batch_engine.cu).
+// Ensemble reductions (trajectories.cpp:17-22, 82-83): the device-side pairwise bracket over a
+// block's completed trajectories (K7, used by qsg_mcsolve) and the host combine of per-block sums
+// gathered from several devices or ranks (qsg_ensemble_combine).
 #include <vector>
 
 #include "qsg_internal.h"
+#include "ensemble.h"
 
 using namespace qsg;
+
+namespace qsg {
+
+// Completed-trajectory list, in index order (run_ensemble keeps the completed ones, :60-73).
+// One block: a chunked exclusive scan over the status flags.
+__global__ void __launch_bounds__(1024) ok_compact_kernel(const int* __restrict__ status, long long n,
+                                                          int* __restrict__ ok_idx, long long* __restrict__ n_ok) {
+  __shared__ int part[1024];
+  __shared__ long long base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (long long c0 = 0; c0 < n; c0 += 1024) {
+    const long long i = c0 + threadIdx.x;
+    const int ok = i < n && status[i] == kDone;
+    part[threadIdx.x] = ok;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const int v = threadIdx.x >= static_cast<unsigned>(o) ? part[threadIdx.x - o] : 0;
+      __syncthreads();
+      part[threadIdx.x] += v;
+      __syncthreads();
+    }
+    if (ok) ok_idx[base + part[threadIdx.x] - 1] = static_cast<int>(i);
+    __syncthreads();
+    if (threadIdx.x == 1023) base += part[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_ok = base;
+}
+
+// pairwise_sum(m, lo, hi) of trajectories.cpp:17-22 for value index v: leaves are whole
+// trajectory matrices, the split is lo + (hi - lo)/2, and each node is left + right.
+__device__ double2 bracket_dev(const double2* __restrict__ per, const int* __restrict__ ok, long long lo,
+                               long long hi, long long nv, long long v) {
+  if (hi - lo == 1) return per[static_cast<long long>(ok[lo]) * nv + v];
+  const long long mid = lo + (hi - lo) / 2;
+  const double2 l = bracket_dev(per, ok, lo, mid, nv, v);
+  const double2 r = bracket_dev(per, ok, mid, hi, nv, v);
+  return make_double2(l.x + r.x, l.y + r.y);
+}
+
+__global__ void bracket_sums_kernel(const double2* __restrict__ per, const int* __restrict__ ok,
+                                    const long long* __restrict__ n_ok, const long long* __restrict__ lo,
+                                    const long long* __restrict__ hi, int n_ranges, long long nv,
+                                    double2* __restrict__ out) {
+  const long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const int r = blockIdx.y;
+  if (v >= nv) return;
+  // hi < 0: up to the end of the completed list
+  const long long a = n_ranges > 0 ? lo[r] : 0, b = n_ranges > 0 && hi[r] >= 0 ? hi[r] : *n_ok;
+  out[static_cast<long long>(r) * nv + v] = b > a ? bracket_dev(per, ok, a, b, nv, v) : make_double2(0.0, 0.0);
+}
+
+cudaError_t device_bracket_sums(const double2* per, const int* status, long long n_sys, long long nv,
+                                int n_ranges, const long long* range_lo, const long long* range_hi,
+                                cudaStream_t s, long long& n_ok, std::vector<double2>& sums) {
+  cudaError_t e;
+  DevBuf ok, nok, dlo, dhi, out;
+  const int nr = n_ranges > 0 ? n_ranges : 1;
+  if ((e = ok.alloc(sizeof(int) * std::max(1LL, n_sys), s)) || (e = nok.alloc(sizeof(long long), s)) ||
+      (e = out.alloc(sizeof(double2) * nv * nr, s)))
+    return e;
+  if (n_ranges > 0 && ((e = upload(dlo, range_lo, sizeof(long long) * n_ranges, s)) ||
+                       (e = upload(dhi, range_hi, sizeof(long long) * n_ranges, s))))
+    return e;
+  ok_compact_kernel<<<1, 1024, 0, s>>>(status, n_sys, ok.as<int>(), nok.as<long long>());
+  const dim3 grid(static_cast<unsigned>((nv + 127) / 128), static_cast<unsigned>(nr));
+  bracket_sums_kernel<<<grid, 128, 0, s>>>(per, ok.as<int>(), nok.as<long long>(), dlo.as<long long>(),
+                                           dhi.as<long long>(), n_ranges, nv, out.as<double2>());
+  sums.resize(static_cast<size_t>(nv * nr));
+  if ((e = cudaGetLastError()) ||
+      (e = cudaMemcpyAsync(&n_ok, nok.p, sizeof(long long), cudaMemcpyDeviceToHost, s)) ||
+      (e = cudaMemcpyAsync(sums.data(), out.p, sizeof(double2) * nv * nr, cudaMemcpyDeviceToHost, s)) ||
+      (e = cudaStreamSynchronize(s)))
+    return e;
+  return cudaSuccess;
+}
+
+}  // namespace qsg
 
 namespace {
 

@@ -3,6 +3,7 @@
 // runs the device engines through the C-ABI (include/qsg.h). No CPU integration path exists.
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -375,24 +376,72 @@ TrajectoryEnsembleResult mcsolve(const TimeDependentOperator& h, const QuantumOb
     const long v = e ? std::atol(e) : 0;
     return v > 0 ? v : 256L;
   }();
-  std::vector<Complex> per(static_cast<size_t>(ntraj * blk));
+  // Shards: whole subtrees of the pairwise bracket (trajectories.cpp:17-22), so every shard's
+  // device-side subtree sums combine into exactly the single-device mean (ensemble_shards).
+  const std::vector<EnsembleShard> shards = ensemble_shards(ntraj, nd);
+  // per-trajectory expectations come back when stored, or when several shards might need the
+  // host bracket (a failed trajectory shifts the bracket over the completed list)
+  const bool fetch_per = ens.store_per_traj || nd > 1;
+  std::vector<Complex> per(fetch_per ? static_cast<size_t>(ntraj * blk) : 0);
   std::vector<int32_t> failed(static_cast<size_t>(ntraj)), jcount(static_cast<size_t>(ntraj));
   std::vector<double> ftime(static_cast<size_t>(ntraj)), jtime(static_cast<size_t>(ntraj * kJumpCap));
   std::vector<int32_t> jch(static_cast<size_t>(ntraj * kJumpCap));
   std::vector<int64_t> tstats(static_cast<size_t>(ntraj * 3));
+  std::vector<std::vector<Complex>> leaf_sums(static_cast<size_t>(nd));
   std::vector<Complex> bsum(static_cast<size_t>(std::max<long>(1, blk)) * static_cast<size_t>(nd));
   std::vector<int64_t> nok(static_cast<size_t>(nd));
   std::vector<qsg_status> rcs(static_cast<size_t>(nd), QSG_OK);
   std::vector<std::string> errs(static_cast<size_t>(nd));
   std::vector<double> dev_ms(static_cast<size_t>(nd));
-  // contiguous trajectory blocks per device (trajectory i always uses RngStream(seed, i))
+  // NCCL communicator over distinct devices (the all-gather of leaf sums); QSG_MC_NCCL=1 uses it
+  // for a single device too. Duplicate device ids run one context per shard and combine on the host.
+  std::vector<qsg_comm*> comms;
+  bool distinct = true;
+  for (int i = 0; i < nd; ++i)
+    for (int j = 0; j < i; ++j) distinct = distinct && devs[static_cast<size_t>(i)] != devs[static_cast<size_t>(j)];
+  const char* force = std::getenv("QSG_MC_NCCL");
+  if (distinct && (nd > 1 || (force && force[0] == '1'))) {
+    comms.assign(static_cast<size_t>(nd), nullptr);
+    check(qsg_comm_init_all(nd, devs.data(), comms.data()));
+  }
+  struct CommGuard {
+    std::vector<qsg_comm*>& c;
+    ~CommGuard() {
+      for (auto* x : c) qsg_comm_destroy(x);
+    }
+  } comm_guard{comms};
+  std::vector<std::vector<Complex>> gathered(static_cast<size_t>(nd));
+  int max_leaves = 0;
+  for (const auto& sh : shards) max_leaves = std::max(max_leaves, static_cast<int>(sh.leaves.size()));
+  const long gcount = 2 * (2 + static_cast<long>(max_leaves) * blk);  // doubles per rank in the gather
   auto run = [&](int k) {
-    const long b = ntraj * k / nd, e = ntraj * (k + 1) / nd;
+    const EnsembleShard& sh = shards[static_cast<size_t>(k)];
+    const long b = sh.begin, e = sh.end;
+    if (e <= b && comms.empty()) return;
     try {
-      qsg_ctx* ctx = device_ctx(devs[static_cast<size_t>(k)]);
+      // one context per shard (own stream and events): shards on the same device do not share one
+      qsg_ctx* ctx = comms.empty() ? nullptr : qsg_comm_ctx(comms[static_cast<size_t>(k)]);
+      qsg_ctx* own = nullptr;
+      if (!ctx) {
+        check(qsg_ctx_create(devs[static_cast<size_t>(k)], &own));
+        ctx = own;
+      }
+      struct CtxGuard {
+        qsg_ctx* c;
+        ~CtxGuard() {
+          if (c) qsg_ctx_destroy(c);
+        }
+      } ctx_guard{own};
       DeviceGenerator gen(ctx, heff, Complex(0, -1));
+      std::vector<int64_t> rlo, rhi;  // leaves as positions in the shard's completed list (valid when none failed)
+      for (const auto& lf : sh.leaves) {
+        rlo.push_back(lf.first - b);
+        rhi.push_back(lf.second - b);
+      }
+      auto& ls = leaf_sums[static_cast<size_t>(k)];
+      ls.assign(static_cast<size_t>(std::max<long>(1, blk)) * sh.leaves.size(), Complex(0, 0));
       qsg_mc_out out{};
-      out.per_traj_expect = reinterpret_cast<double*>(per.data() + b * blk);
+      out.per_traj_expect = fetch_per ? reinterpret_cast<double*>(per.data() + b * blk) : nullptr;
       out.block_sum = reinterpret_cast<double*>(bsum.data() + k * std::max<long>(1, blk));
       out.n_ok = &nok[static_cast<size_t>(k)];
       out.failed = failed.data() + b;
@@ -402,13 +451,32 @@ TrajectoryEnsembleResult mcsolve(const TimeDependentOperator& h, const QuantumOb
       out.jump_time = jtime.data() + b * kJumpCap;
       out.jump_channel = jch.data() + b * kJumpCap;
       out.jump_capacity = kJumpCap;
+      out.n_ranges = static_cast<int32_t>(sh.leaves.size());
+      out.range_lo = rlo.data();
+      out.range_hi = rhi.data();
+      out.range_sums = reinterpret_cast<double*>(ls.data());
       qsg_timing tm{};
-      rcs[static_cast<size_t>(k)] =
-          qsg_mcsolve(ctx, &gen.g, static_cast<int32_t>(cv.size()), cv.data(), static_cast<int32_t>(ne), ev.data(),
-                      psi0.dim(), reinterpret_cast<const double*>(y0.data()), tlist.data(), nt, params.data(),
-                      static_cast<int32_t>(params.size()), ens.seed, b, e, &o, &out, &tm);
+      if (e > b)
+        rcs[static_cast<size_t>(k)] =
+            qsg_mcsolve(ctx, &gen.g, static_cast<int32_t>(cv.size()), cv.data(), static_cast<int32_t>(ne),
+                        ev.data(), psi0.dim(), reinterpret_cast<const double*>(y0.data()), tlist.data(), nt,
+                        params.data(), static_cast<int32_t>(params.size()), ens.seed, b, e, &o, &out, &tm);
       if (rcs[static_cast<size_t>(k)] != QSG_OK) errs[static_cast<size_t>(k)] = qsg_last_error();
       dev_ms[static_cast<size_t>(k)] = tm.kernel_ms;
+      if (!comms.empty()) {  // NCCL all-gather of [n_ok, n_leaves, leaf sums] from every shard
+        std::vector<Complex> send(static_cast<size_t>(gcount / 2), Complex(0, 0));
+        send[0] = Complex(static_cast<double>(nok[static_cast<size_t>(k)]), rcs[static_cast<size_t>(k)] == QSG_OK ? 0.0 : 1.0);
+        send[1] = Complex(static_cast<double>(sh.leaves.size()), 0.0);
+        std::copy(ls.begin(), ls.end(), send.begin() + 2);
+        auto& g = gathered[static_cast<size_t>(k)];
+        g.resize(static_cast<size_t>(gcount / 2 * nd));
+        const qsg_status gs = qsg_comm_allgather(comms[static_cast<size_t>(k)], reinterpret_cast<const double*>(send.data()),
+                                                 gcount, reinterpret_cast<double*>(g.data()));
+        if (gs != QSG_OK && rcs[static_cast<size_t>(k)] == QSG_OK) {
+          rcs[static_cast<size_t>(k)] = gs;
+          errs[static_cast<size_t>(k)] = qsg_last_error();
+        }
+      }
     } catch (const std::exception& ex) {
       rcs[static_cast<size_t>(k)] = QSG_CUDA_ERROR;
       errs[static_cast<size_t>(k)] = ex.what();
@@ -432,27 +500,59 @@ TrajectoryEnsembleResult mcsolve(const TimeDependentOperator& h, const QuantumOb
   r.ntraj = static_cast<int>(ntraj);
   r.master_seed = ens.seed;
   for (double ms : dev_ms) r.device_ms = std::max(r.device_ms, ms);
-  std::vector<DenseMatrix> mats(static_cast<size_t>(ntraj));
+  std::vector<DenseMatrix> mats(fetch_per ? static_cast<size_t>(ntraj) : 0);
   std::vector<const DenseMatrix*> ok;
+  long n_ok = 0;
   for (long i = 0; i < ntraj; ++i) {
     if (failed[static_cast<size_t>(i)]) {
       ++r.failed_trajectories;
       r.stats.warnings.push_back("trajectory " + std::to_string(i) + " failed: IntegrationFailure");
       continue;
     }
-    DenseMatrix m(ne, nt);
-    std::copy(per.begin() + i * blk, per.begin() + (i + 1) * blk, m.data());
-    mats[static_cast<size_t>(i)] = std::move(m);
-    ok.push_back(&mats[static_cast<size_t>(i)]);
+    ++n_ok;
+    if (fetch_per) {
+      DenseMatrix m(ne, nt);
+      std::copy(per.begin() + i * blk, per.begin() + (i + 1) * blk, m.data());
+      mats[static_cast<size_t>(i)] = std::move(m);
+      ok.push_back(&mats[static_cast<size_t>(i)]);
+    }
     r.traj_indices.push_back(static_cast<int>(i));
     r.stats.steps += tstats[static_cast<size_t>(3 * i)];
     r.stats.rejected += tstats[static_cast<size_t>(3 * i + 1)];
     r.stats.rhs_evals += tstats[static_cast<size_t>(3 * i + 2)];
   }
-  require(!ok.empty(), ErrorCode::EnsembleFailure, "every trajectory failed");
-  r.mean_expect = pairwise_sum(ok, 0, ok.size());
-  for (long i = 0; i < r.mean_expect.size(); ++i)
-    r.mean_expect.data()[i] = r.mean_expect.data()[i] / Complex(static_cast<double>(ok.size()), 0.0);
+  require(n_ok > 0, ErrorCode::EnsembleFailure, "every trajectory failed");
+  r.mean_expect = DenseMatrix(ne, nt);
+  if (blk > 0) {
+    std::vector<Complex> mean(static_cast<size_t>(blk));
+    if (nd == 1) {
+      // the device bracket over the block's completed list is the reference's pairwise_sum
+      for (long i = 0; i < blk; ++i) mean[static_cast<size_t>(i)] = bsum[static_cast<size_t>(i)] / Complex(static_cast<double>(n_ok), 0.0);
+    } else if (r.failed_trajectories == 0) {
+      // every shard's leaves are whole bracket subtrees: combine them (NCCL-gathered when a
+      // communicator exists, else straight from the shard threads)
+      std::vector<int64_t> lb, le;
+      std::vector<Complex> sums;
+      for (int k = 0; k < nd; ++k) {
+        const EnsembleShard& sh = shards[static_cast<size_t>(k)];
+        const Complex* src = leaf_sums[static_cast<size_t>(k)].data();
+        if (!comms.empty()) src = gathered[0].data() + static_cast<size_t>(gcount / 2 * k) + 2;
+        for (size_t j = 0; j < sh.leaves.size(); ++j) {
+          lb.push_back(sh.leaves[j].first);
+          le.push_back(sh.leaves[j].second);
+          sums.insert(sums.end(), src + j * blk, src + (j + 1) * blk);
+        }
+      }
+      check(qsg_ensemble_combine(static_cast<int32_t>(lb.size()), lb.data(), le.data(),
+                                 reinterpret_cast<const double*>(sums.data()), blk, n_ok,
+                                 reinterpret_cast<double*>(mean.data())));
+    } else {
+      // failures shift the bracket over the completed list: the host pairwise over all shards
+      DenseMatrix tot = pairwise_sum(ok, 0, ok.size());
+      for (long i = 0; i < blk; ++i) mean[static_cast<size_t>(i)] = tot.data()[i] / Complex(static_cast<double>(n_ok), 0.0);
+    }
+    std::copy(mean.begin(), mean.end(), r.mean_expect.data());
+  }
   for (int i : r.traj_indices) {
     std::vector<JumpEvent> jr;
     const int cnt = jcount[static_cast<size_t>(i)];
@@ -492,6 +592,36 @@ TrajectoryEnsembleResult mcsolve(const TimeDependentOperator& h, const QuantumOb
     if (ens.store_per_traj) r.per_traj_expect.push_back(mats[static_cast<size_t>(i)]);
   }
   return r;
+}
+
+std::vector<EnsembleShard> ensemble_shards(long ntraj, int nshards) {
+  // leaves: the bracket's nodes at depth D (split lo + (hi - lo)/2, trajectories.cpp:17-22), with
+  // D = log2(nshards) for a power of two and 3 levels deeper otherwise, so shards stay balanced
+  int D = 0;
+  while ((1 << D) < nshards) ++D;
+  if ((1 << D) != nshards) D += 3;
+  std::vector<std::pair<long, long>> leaves;
+  std::function<void(long, long, int)> rec = [&](long lo, long hi, int d) {
+    if (d == 0 || hi - lo <= 1) {
+      leaves.emplace_back(lo, hi);
+      return;
+    }
+    const long mid = lo + (hi - lo) / 2;
+    rec(lo, mid, d - 1);
+    rec(mid, hi, d - 1);
+  };
+  rec(0, ntraj, D);
+  std::vector<EnsembleShard> out(static_cast<size_t>(nshards));
+  size_t j = 0;
+  for (int k = 0; k < nshards; ++k) {
+    const long target = ntraj * (k + 1) / nshards;  // cumulative trajectories at this shard's end
+    EnsembleShard& sh = out[static_cast<size_t>(k)];
+    sh.begin = j < leaves.size() ? leaves[j].first : ntraj;
+    while (j < leaves.size() && (leaves[j].second <= target || k == nshards - 1)) sh.leaves.push_back(leaves[j++]);
+    if (sh.leaves.empty() && j < leaves.size()) sh.leaves.push_back(leaves[j++]);
+    sh.end = sh.leaves.empty() ? sh.begin : sh.leaves.back().second;
+  }
+  return out;
 }
 
 namespace {

@@ -253,7 +253,7 @@ qsg_status qsg_model_mcsolve(qsg_model* m, int32_t n_devices, const int32_t* dev
                              int64_t n_t, const double* params, int32_t n_params, uint64_t seed, int32_t ntraj,
                              const qsg_solve_opts* opts, double* mean, double* per_traj, int64_t* traj_stats,
                              int32_t* n_jumps, double* jump_time, int32_t* jump_channel, int32_t jump_cap,
-                             int32_t* n_failed, double* device_ms) {
+                             int32_t* n_failed, double* device_ms, double* stddev) {
   try {
     SolveOptions o = from_opts(opts);
     EnsembleOptions ens;
@@ -282,6 +282,10 @@ qsg_status qsg_model_mcsolve(qsg_model* m, int32_t n_devices, const int32_t* dev
     }
     if (n_failed) *n_failed = r.failed_trajectories;
     if (device_ms) *device_ms = r.device_ms;
+    if (stddev) {  // trajectories.cpp:94-104
+      const std::vector<double> sd = ensemble_stddev(r);
+      std::memcpy(stddev, sd.data(), sd.size() * sizeof(double));
+    }
     return QSG_OK;
   } catch (const std::exception& e) {
     return fail(e);

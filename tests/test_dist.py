@@ -12,7 +12,8 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_2504_21440_b200.dist import combine_mean, gather_block_sums, shard_range
+from paper_2504_21440_b200.dist import (combine_leaves, combine_mean, ensemble_shards, gather_block_sums,
+                                        gather_leaf_sums, shard_range)
 
 NTRAJ, NE, NT = 10000, 1, 100
 
@@ -49,15 +50,17 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     data = synthetic()
-    b, e = shard_range(NTRAJ, rank, world)
-    bs = pairwise(list(data[b:e]), 0, e - b)
-    sums, counts = gather_block_sums(bs, e - b, world)
-    mean = combine_mean(NTRAJ, world, sums, counts)
+    shards = ensemble_shards(NTRAJ, world)
+    b, e, leaves = shards[rank]
+    # per-leaf pairwise sums, as qsg_mcsolve's range_sums return them
+    ls = [pairwise(list(data[lo:hi]), 0, hi - lo) for lo, hi in leaves]
+    sums, counts = gather_leaf_sums(ls, e - b, max(len(s[2]) for s in shards), world)
+    mean = combine_leaves(NTRAJ, world, sums, counts)
     q.put((rank, mean, counts))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_sharded_combine_bitwise_equals_single_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -72,7 +75,7 @@ def test_sharded_combine_bitwise_equals_single_process(world):
     data = synthetic()
     ref = cdiv(pairwise(list(data), 0, NTRAJ), NTRAJ)
     for rank, mean, counts in out:
-        assert counts == [NTRAJ // 2, NTRAJ // 2]
+        assert sum(counts) == NTRAJ and max(counts) - min(counts) <= NTRAJ // (8 * world) + 1
         assert np.array_equal(mean.view(np.float64), ref.view(np.float64)), rank
 
 
@@ -95,3 +98,20 @@ def test_misaligned_blocks_rejected():
     import paper_2504_21440_b200 as q
     with pytest.raises(q.QsgError):
         q.ensemble_combine([(0, 3), (3, 10)], [np.ones((1, 2)), np.ones((1, 2))], 10)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5, 6, 7, 8])
+def test_ensemble_shards_tile_and_balance(world):
+    """Shards are contiguous, tile [0, N), are made of whole bracket subtrees, and stay balanced
+    for any world size (non-power-of-two worlds)."""
+    shards = ensemble_shards(NTRAJ, world)
+    assert shards[0][0] == 0 and shards[-1][1] == NTRAJ
+    for (b0, e0, _), (b1, e1, _) in zip(shards, shards[1:]):
+        assert e0 == b1
+    sizes = [e - b for b, e, _ in shards]
+    assert max(sizes) - min(sizes) <= NTRAJ // (8 * world) + 2
+    data = synthetic()[:, :, :3]
+    sums = [[pairwise(list(data[lo:hi]), 0, hi - lo) for lo, hi in lv] for _, _, lv in shards]
+    mean = combine_leaves(NTRAJ, world, sums, sizes)
+    ref = cdiv(pairwise(list(data), 0, NTRAJ), NTRAJ)
+    assert np.array_equal(mean.view(np.float64), ref.view(np.float64))

@@ -91,3 +91,17 @@ def test_cpp_ssesolve_smesolve_match_oracle():
     ref = O.Model("jc_sme", *prm).smesolve(t2, 7, 6, n_det=2, dt_max=2e-3)
     for i in range(6):
         assert normwise_rel(dev["per_traj"][i], ref["per_traj"][i]) <= TOL, i
+
+
+def test_ssesolve_without_e_ops(ctx):
+    """Empty e_ops is legal (the reference stores nothing per trajectory): the call must not write
+    past the caller's zero-length buffers, and the measurement records still match the oracle."""
+    m = O.Model("jc_sse", 6, 1.0, 1.0, 0.1, 0.3)
+    t = np.linspace(0.0, 0.5, 6)
+    G = oracle_generator(ctx, m, "se")
+    sc = [csr_from_oracle(m, O.C_OP, k) for k in range(m.n_cops)]
+    guard = np.full(64, 7.25)
+    dev = q.ssesolve(ctx, G, sc, [], m.dim, m.psi0(), t, 31, 0, 8, dt_max=1e-3, store_measurement=True)
+    assert dev["per_traj"].size == 0 and np.all(guard == 7.25)
+    ref = m.ssesolve(t, 31, 8, dt_max=1e-3, store_measurement=True)
+    assert np.max(np.abs(dev["increments"] - ref["increments"])) <= 1e-13 * np.max(np.abs(ref["increments"]))
