@@ -80,10 +80,15 @@ class ClockSampler:
         self.p = None
 
     def __enter__(self):
+        # 50 ms period; wait for the first sample so the sampler is live before the timed region
+        import selectors
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            sel = selectors.DefaultSelector()
+            sel.register(self.p.stdout, selectors.EVENT_READ)
+            self.first = self.p.stdout.readline() if sel.select(timeout=5.0) else ""
         except Exception:
             self.p = None
         return self
@@ -94,7 +99,7 @@ class ClockSampler:
             self.p.terminate()
             try:
                 out, _ = self.p.communicate(timeout=5)
-                self.lines = [l for l in out.splitlines() if l.strip()]
+                self.lines = [l for l in out.splitlines() if l.strip()]  # the pre-roll sample is excluded
             except Exception:
                 self.p.kill()
 

@@ -220,6 +220,11 @@ qsg_status common_setup(qsg_ctx* ctx, const qsg_generator* G, long long n, const
   }
   P.n = static_cast<int>(n);
   P.gen = make_devgen(G, batch_codes());
+  // generator terms that carry a key-aligned store are read through it (ka_row_slot) unless
+  // QSG_BATCH_KA=0
+  if (const char* e = std::getenv("QSG_BATCH_KA"))
+    if (e[0] == '0')
+      for (int k = 0; k < P.gen.n_terms; ++k) P.gen.A[k].ka_nval = 0;
   P.atol = opts ? opts->abstol : 1e-8;
   P.rtol = opts ? opts->reltol : 1e-6;
   if (!(P.atol > 0 && P.rtol > 0)) {

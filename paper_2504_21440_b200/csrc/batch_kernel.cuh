@@ -178,10 +178,63 @@ __device__ __forceinline__ double2 dense_at(const Ctx<BS, NA>& C, int c, int s, 
   return o;
 }
 
-// one row of a SELL operator applied to slot s of a gathered vector (plain or dictionary-coded
-// store, engine.cuh DevSell); the row's entries are broadcast to the slots of the warp
+// One row of a key-aligned store (engine.cuh DevSell::ka_*; the grid engine's ka_row) when a warp
+// holds one slice, i.e. 32 consecutive rows of one slot: the slice block's words are read at
+// warp-uniform addresses through L1 (the whole store is a few tens of KB here), the value groups
+// sum their gathers before one multiply, and no per-entry column or value is loaded.
 template <class XF>
+__device__ __forceinline__ double2 ka_row_slot(const DevSell& A, int row, XF&& xf) {
+  const unsigned bit = 1u << (row & 31);
+  const unsigned* __restrict__ w = reinterpret_cast<const unsigned*>(A.ka_blk) + 4ull * __ldg(A.ka_off + (row >> 5));
+  const uint4 h = __ldg(reinterpret_cast<const uint4*>(w));
+  const int G = static_cast<int>(h.x), NN = static_cast<int>(h.y), Pu = static_cast<int>(h.z);
+  const unsigned* kw_p = w + kKaHdrWords + G;
+  const unsigned* mk_p = kw_p + Pu;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int g = 0; g < G; ++g) {
+    const unsigned gw = __ldg(w + kKaHdrWords + g);
+    const int cnt = static_cast<int>(gw >> 16);
+    double2 sum = make_double2(0.0, 0.0);
+    for (int c = 0; c < cnt; c += 4) {
+      unsigned kw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) kw[u] = c + u < cnt ? __ldg(kw_p + u) : 0x80000000u;
+      double2 x[4];
+      int q = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool part = static_cast<int>(kw[u]) < 0;
+        const unsigned m = part ? (c + u < cnt ? __ldg(mk_p + q) : 0u) : 0xffffffffu;
+        q += (part && c + u < cnt) ? 1 : 0;
+        x[u] = (m & bit) ? xf((row ^ static_cast<int>(kw[u])) & 0x7fffffff) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) sum = cadd(sum, x[u]);
+      kw_p += 4;
+      mk_p += q;
+    }
+    kw_p += cnt - ((cnt + 3) & ~3);
+    cfma(__ldg(A.ka_val + (gw & 0xffffu)), sum, acc);
+  }
+  const unsigned* ep = mk_p;
+  for (int e = 0; e < NN; ++e, ep += kKaNonUniWords) {
+    const unsigned key = __ldg(ep), msk = __ldg(ep + 1);
+    if (msk & bit) {
+      const unsigned short vid = __ldg(reinterpret_cast<const unsigned short*>(ep + 2) + (row & 31));
+      cfma(__ldg(A.ka_val + vid), xf(row ^ static_cast<int>(key)), acc);
+    }
+  }
+  return acc;
+}
+
+// one row of a SELL operator applied to slot s of a gathered vector (plain or dictionary-coded
+// store, engine.cuh DevSell); the row's entries are broadcast to the slots of the warp.
+// KA: the caller's warp holds whole slices of one slot, so a key-aligned store may be used.
+template <bool KA = false, class XF>
 __device__ __forceinline__ double2 sell_row_slot(const DevSell& A, int row, XF&& xf) {
+  if constexpr (KA) {
+    if (A.ka_nval > 0) return ka_row_slot(A, row, xf);
+  }
   const int sl = row >> 5, ln = row & 31;
   const int len = __ldg(A.rowlen + row);
   double2 acc = make_double2(0.0, 0.0);
@@ -228,12 +281,12 @@ __device__ __forceinline__ double2 sell_row_slot(const DevSell& A, int row, XF&&
   return acc;
 }
 
-template <class XF>
+template <bool KA = false, class XF>
 __device__ __forceinline__ double2 gen_row_slot(const DevGen& g, const double* params, int row, double t,
                                                 XF&& xf) {
-  double2 s = sell_row_slot(g.A[0], row, xf);
+  double2 s = sell_row_slot<KA>(g.A[0], row, xf);
   for (int k = 1; k < g.n_terms; ++k) {
-    const double2 sk = sell_row_slot(g.A[k], row, xf);
+    const double2 sk = sell_row_slot<KA>(g.A[k], row, xf);
     s = cadd(s, cmul(coeff_eval(g.c[k], params, t), sk));
   }
   return s;
@@ -501,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       const double* prm = slot_params(P, S[sl]);
       if (ph == START) {
         rows([&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, t0, [&](int c) { return C.ldx(Y, c, sl); });
+          const double2 k = gen_row_slot<true>(P.gen, prm, r, t0, [&](int c) { return C.ldx(Y, c, sl); });
           C.st(K1, r, sl, k);
           const double2 yy = C.ld(Y, r, sl);
           const double sc = atol + rtol * cabs_(yy);
@@ -512,7 +565,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
         rows_pf((1u << Y) | (1u << K1), [&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, t + c2 * hh, [&](int c) {
+          const double2 k = gen_row_slot<true>(P.gen, prm, r, t + c2 * hh, [&](int c) {
             const double2 a = C.ldx(Y, c, sl), q = C.ldx(K1, c, sl);
             return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
           });
@@ -659,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       if (ph2 == START) {
         const double h0 = S[sl].h0;
         rows([&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, t0 + h0, [&](int c) {
+          const double2 k = gen_row_slot<true>(P.gen, prm, r, t0 + h0, [&](int c) {
             const double2 a = C.ldx(Y, c, sl), q = C.ldx(K1, c, sl);
             return make_double2(a.x + h0 * q.x, a.y + h0 * q.y);
           });
@@ -672,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
         rows_pf((1u << Y) | (1u << K1) | (1u << K2), [&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, t + c3 * hh, [&](int c) { return C.ldx(SA, c, sl); });
+          const double2 k = gen_row_slot<true>(P.gen, prm, r, t + c3 * hh, [&](int c) { return C.ldx(SA, c, sl); });
           const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl);
           C.st(K3, r, sl, k);
           C.st(SB, r, sl, make_double2(yy.x + hh * (a41 * q1.x + a42 * q2.x + a43 * k.x),
@@ -712,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
         rows_pf((1u << Y) | (1u << K1) | (1u << K2) | (1u << K3), [&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, t + c4 * hh, [&](int c) { return C.ldx(SB, c, sl); });
+          const double2 k = gen_row_slot<true>(P.gen, prm, r, t + c4 * hh, [&](int c) { return C.ldx(SB, c, sl); });
           const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl), q3 = C.ld(K3, r, sl);
           C.st(K4, r, sl, k);
           C.st(SA, r, sl, make_double2(yy.x + hh * (a51 * q1.x + a52 * q2.x + a53 * q3.x + a54 * k.x),
@@ -722,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         // restart: integ.start(jump_t, psi, tf, h_current) (trajectories.cpp:202-203)
         const double tj = S[sl].jump_t;
         rows([&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, tj, [&](int c) { return C.ldx(SC, c, sl); });
+          const double2 k = gen_row_slot<true>(P.gen, prm, r, tj, [&](int c) { return C.ldx(SC, c, sl); });
           C.st(K1, r, sl, k);
           C.st(Y, r, sl, C.ld(SC, r, sl));
         });
@@ -753,7 +806,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       const double hh = S[sl].hh, t = S[sl].t;
       using namespace dp;
       rows_pf((1u << Y) | (1u << K1) | (1u << K2) | (1u << K3) | (1u << K4), [&](int r) {
-        const double2 k = gen_row_slot(P.gen, prm, r, t + c5 * hh, [&](int c) { return C.ldx(SA, c, sl); });
+        const double2 k = gen_row_slot<true>(P.gen, prm, r, t + c5 * hh, [&](int c) { return C.ldx(SA, c, sl); });
         const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q2 = C.ld(K2, r, sl), q3 = C.ld(K3, r, sl),
                       q4 = C.ld(K4, r, sl);
         C.st(K5, r, sl, k);
@@ -768,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       const double hh = S[sl].hh, t = S[sl].t;
       using namespace dp;
       rows_pf((1u << Y) | (1u << K1) | (1u << K3) | (1u << K4) | (1u << K5), [&](int r) {
-        const double2 k = gen_row_slot(P.gen, prm, r, t + hh, [&](int c) { return C.ldx(SB, c, sl); });
+        const double2 k = gen_row_slot<true>(P.gen, prm, r, t + hh, [&](int c) { return C.ldx(SB, c, sl); });
         const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl), q3 = C.ld(K3, r, sl), q4 = C.ld(K4, r, sl),
                       q5 = C.ld(K5, r, sl);
         C.st(K6, r, sl, k);
@@ -787,7 +840,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
         rows_pf((1u << Y) | (1u << Y1) | (1u << K1) | (1u << K3) | (1u << K4) | (1u << K5) | (1u << K6), [&](int r) {
-          const double2 k = gen_row_slot(P.gen, prm, r, t + hh, [&](int c) { return C.ldx(Y1, c, sl); });
+          const double2 k = gen_row_slot<true>(P.gen, prm, r, t + hh, [&](int c) { return C.ldx(Y1, c, sl); });
           const double2 yy = C.ld(Y, r, sl), y1 = C.ld(Y1, r, sl), q1 = C.ld(K1, r, sl), q3 = C.ld(K3, r, sl),
                         q4 = C.ld(K4, r, sl), q5 = C.ld(K5, r, sl), q6 = C.ld(K6, r, sl);
           C.st(K7, r, sl, k);

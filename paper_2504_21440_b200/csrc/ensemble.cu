@@ -38,14 +38,45 @@ __global__ void __launch_bounds__(1024) ok_compact_kernel(const int* __restrict_
 }
 
 // pairwise_sum(m, lo, hi) of trajectories.cpp:17-22 for value index v: leaves are whole
-// trajectory matrices, the split is lo + (hi - lo)/2, and each node is left + right.
-__device__ double2 bracket_dev(const double2* __restrict__ per, const int* __restrict__ ok, long long lo,
-                               long long hi, long long nv, long long v) {
-  if (hi - lo == 1) return per[static_cast<long long>(ok[lo]) * nv + v];
-  const long long mid = lo + (hi - lo) / 2;
-  const double2 l = bracket_dev(per, ok, lo, mid, nv, v);
-  const double2 r = bracket_dev(per, ok, mid, hi, nv, v);
-  return make_double2(l.x + r.x, l.y + r.y);
+// trajectory matrices, the split is lo + (hi - lo)/2, and each node is left + right. Evaluated
+// with an explicit stack (a statically sized frame: device recursion would overrun the default
+// per-thread stack at ~2^12 trajectories).
+__device__ double2 bracket_dev(const double2* __restrict__ per, const int* __restrict__ ok, long long lo0,
+                               long long hi0, long long nv, long long v) {
+  constexpr int kDepth = 64;
+  long long los[kDepth], his[kDepth];
+  double2 left[kDepth];
+  unsigned char st[kDepth];
+  int sp = 0;
+  los[0] = lo0;
+  his[0] = hi0;
+  st[0] = 0;
+  double2 ret = make_double2(0.0, 0.0);
+  for (;;) {
+    const long long lo = los[sp], hi = his[sp];
+    if (st[sp] == 0 && hi - lo == 1) {
+      ret = per[static_cast<long long>(ok[lo]) * nv + v];
+    } else if (st[sp] == 0) {  // descend left
+      st[sp] = 1;
+      ++sp;
+      los[sp] = lo;
+      his[sp] = lo + (hi - lo) / 2;
+      st[sp] = 0;
+      continue;
+    } else if (st[sp] == 1) {  // left done: keep it, descend right
+      left[sp] = ret;
+      st[sp] = 2;
+      ++sp;
+      los[sp] = lo + (hi - lo) / 2;
+      his[sp] = hi;
+      st[sp] = 0;
+      continue;
+    } else {  // both done
+      ret = make_double2(left[sp].x + ret.x, left[sp].y + ret.y);
+    }
+    if (sp == 0) return ret;
+    --sp;
+  }
 }
 
 __global__ void bracket_sums_kernel(const double2* __restrict__ per, const int* __restrict__ ok,

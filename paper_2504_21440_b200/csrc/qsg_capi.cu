@@ -64,7 +64,7 @@ DevSell sell_view(const qsg_op* op, bool use_codes) {
   v.ka_off = op->ka_off;
   v.ka_blk = op->ka_blk;
   v.ka_val = op->ka_val;
-  v.ka_nval = use_codes ? op->ka_nval : 0;
+  v.ka_nval = op->ka_nval;  // each engine decides whether to read it (grid: st 2; batch: QSG_BATCH_KA)
   v.ka_slot = op->ka_slot;
   return v;
 }
@@ -1007,17 +1007,16 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
       return cuda_fail(e, "coded operator store");
     }
     mark("coded");
-    // key-aligned store for the persistent grid engine, built on request (QSG_KA_STORE=1 or
-    // QSG_KA_SOLVE=1): it is not the default solve path (see run_grid_solve)
-    const char* kst = std::getenv("QSG_KA_STORE");
-    const char* ksv = std::getenv("QSG_KA_SOLVE");
-    if ((kst && kst[0] == '1') || (ksv && ksv[0] == '1')) {
-      if ((e = build_ka_store(op, d_rp.as<int>(), d_col.as<int>(), d_val.as<double2>(), n, s))) {
-        qsg_op_destroy(op);
-        return cuda_fail(e, "key-aligned operator store");
-      }
-      mark("key-aligned");
+  }
+  // key-aligned store, built on request (QSG_KA_STORE=1, or QSG_KA_SOLVE=1 for the grid solver)
+  const char* kst = std::getenv("QSG_KA_STORE");
+  const char* ksv = std::getenv("QSG_KA_SOLVE");
+  if (a->nnz > 0 && ((kst && kst[0] == '1') || (ksv && ksv[0] == '1'))) {
+    if ((e = build_ka_store(op, d_rp.as<int>(), d_col.as<int>(), d_val.as<double2>(), n, s))) {
+      qsg_op_destroy(op);
+      return cuda_fail(e, "key-aligned operator store");
     }
+    mark("key-aligned");
   }
   *out = op;
   return QSG_OK;

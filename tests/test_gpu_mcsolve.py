@@ -256,3 +256,22 @@ def test_ising6_mcsolve_matches_mesolve_3sigma(ctx):
     sd = mc["stddev"][e]
     viol = np.abs(mc["mean"][e].real - om[e].real) > 3 * sd / np.sqrt(2000) + 1e-3
     assert viol.sum() <= 1, np.nonzero(viol)
+
+
+def _pairwise(mats, lo, hi):
+    if hi - lo == 1:
+        return mats[lo].copy()
+    mid = lo + (hi - lo) // 2
+    return _pairwise(mats, lo, mid) + _pairwise(mats, mid, hi)
+
+
+def test_device_bracket_sums_large_ensemble(ctx):
+    """The device bracket (K7) over 5,000 trajectories (13 levels) equals the host pairwise_sum of
+    the per-trajectory data bit for bit, and so do sub-range sums."""
+    m = O.Model("decay2", 0.25)
+    t = np.linspace(0, 40, 21)
+    r = _mc(ctx, m, t, 3, 0, 5000, ranges=[(0, 2500), (2500, 5000), (17, 4099)])
+    per = list(r["per_traj"])
+    assert np.array_equal(r["block_sum"].view(np.float64), _pairwise(per, 0, 5000).view(np.float64))
+    for (lo, hi), s in zip([(0, 2500), (2500, 5000), (17, 4099)], r["range_sums"]):
+        assert np.array_equal(s.view(np.float64), _pairwise(per, lo, hi).view(np.float64))
