@@ -493,7 +493,10 @@ TrajectoryEnsembleResult mcsolve(const TimeDependentOperator& h, const QuantumOb
     if (rcs[static_cast<size_t>(k)] != QSG_OK) {
       if (rcs[static_cast<size_t>(k)] >= 1 && rcs[static_cast<size_t>(k)] <= 12)
         throw Error(static_cast<ErrorCode>(rcs[static_cast<size_t>(k)] - 1), errs[static_cast<size_t>(k)]);
-      throw std::runtime_error("qsim device error: " + errs[static_cast<size_t>(k)]);
+      {
+        const std::string& m = errs[static_cast<size_t>(k)];
+        throw std::runtime_error(m.rfind("qsim device error", 0) == 0 ? m : "qsim device error: " + m);
+      }
     }
   TrajectoryEnsembleResult r;  // run_ensemble bookkeeping (trajectories.cpp:60-91)
   r.times.assign(tlist.begin(), tlist.end());
