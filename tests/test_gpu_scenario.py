@@ -17,6 +17,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 QSIM = os.path.join(ROOT, "paper_2504_21440_b200", "bin", "qsim")
 
 
+def make_tlist(t0, tf, n):
+    """scenario.cpp:378-384: t0 + (tf - t0) * i / (n - 1), not numpy's linspace rounding."""
+    return np.array([t0 + (tf - t0) * float(i) / (n - 1) for i in range(n)])
+
+
 def run(name, tmp_path, *extra):
     r = subprocess.run([QSIM, "run", name, "--out-dir", str(tmp_path), *extra], capture_output=True, text=True,
                        timeout=600)
@@ -43,7 +48,7 @@ def test_qsim_run_ising_mc_2x3(tmp_path):
     tab, j = check_format(csv, side, ["t", "Sz_total_re", "Sz_total_im"])
     assert j["scenario"]["name"] == "ising_mc_2x3" and j["ntraj"] == 200 and j["seed"] == 2025
     assert j["extras"]["completed_trajectories"] == 200 and j["extras"]["failed_trajectories"] == 0
-    t = np.linspace(0.0, 10.0, 100)
+    t = make_tlist(0.0, 10.0, 100)
     ref = O.Model("ising", 2, 3, 1.0, 0.2, 1.0, 1).mcsolve(t, 2025, 200, n_threads=os.cpu_count() or 1)
     assert np.array_equal(tab[:, 0], t)
     assert normwise_rel(tab[:, 1] + 1j * tab[:, 2], ref["mean"][2]) <= 1e-9
@@ -57,7 +62,7 @@ def test_qsim_run_jc_mcsolve_and_overrides(tmp_path):
     csv, side = run("jc_mcsolve", tmp_path, "--ntraj", "40", "--seed", "7")
     tab, j = check_format(csv, side, ["t", "n_cavity_re", "n_cavity_im"])
     assert j["ntraj"] == 40 and j["seed"] == 7 and j["scenario"]["seed"] == 7
-    t = np.linspace(0.0, 314.15926535897933, 1000)
+    t = make_tlist(0.0, 314.15926535897933, 1000)
     ref = O.Model("jc", 10, 1.0, 1.0, 0.1, 0.01, 0.01).mcsolve(t, 7, 40, n_threads=os.cpu_count() or 1)
     assert normwise_rel(tab[:, 1] + 1j * tab[:, 2], ref["mean"][0]) <= 1e-6
 
@@ -65,7 +70,7 @@ def test_qsim_run_jc_mcsolve_and_overrides(tmp_path):
 def test_qsim_run_jc_mesolve(tmp_path):
     csv, side = run("jc_mesolve", tmp_path)
     tab, j = check_format(csv, side, ["t", "n_cavity_re", "n_cavity_im"])
-    t = np.linspace(0.0, 314.15926535897933, 1000)
+    t = make_tlist(0.0, 314.15926535897933, 1000)
     ex, st, _ = O.Model("jc", 10, 1.0, 1.0, 0.1, 0.01, 0.01).mesolve(t)
     assert normwise_rel(tab[:, 1] + 1j * tab[:, 2], ex[0]) <= 1e-6
     assert j["stats"]["rhs_evals"] == 2 + 6 * (j["stats"]["steps"] + j["stats"]["rejected"])
