@@ -165,6 +165,18 @@ __device__ __forceinline__ void grid_value(const double* red, int s, int G, doub
   }
 }
 
+// Grid-wide barrier of the solve: the monotone-counter grid barrier of a cooperative launch, or,
+// when the whole grid is one thread-block cluster (small systems), the hardware cluster barrier
+// (release/acquire at cluster scope; the acquire also invalidates L1, so gathers see the other
+// CTAs' stores).
+__device__ __forceinline__ void sync_all(const GridProblem& P, int G) {
+  if (P.cluster) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    grid_barrier(P.bar, G);
+  }
+}
+
 __device__ __forceinline__ void push_pending(const GridProblem& P, Ctl& c, double theta) {
   c.pend[c.np] = Pending{theta, P.ev_grid[c.next], P.ev_save[c.next]};
   ++c.np;
@@ -623,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
   // observation flush: pass, barrier, CTA-0 commit (double-buffered slots)
   auto flush_obs = [&]() {
     observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
-    grid_barrier(P.bar, G);
+    sync_all(P, G);
     observe_commit(P, c, slots(c.obs_par), G);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -708,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
       red[static_cast<long long>(kSlotD1) * G + rank] = d1;
     }
     if (c.np) observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
-    grid_barrier(P.bar, G);
+    sync_all(P, G);
     if (c.np) observe_commit(P, c, slots(c.obs_par), G);
     grid_value(red, kSlotD0, G, &s_val[0]);
     __syncthreads();
@@ -734,7 +746,7 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     double d2 = start_pass2(P, c, s0, s1);
     d2 = block_sum(d2, s_red);
     if (threadIdx.x == 0) red[static_cast<long long>(kSlotD2) * G + rank] = d2;
-    grid_barrier(P.bar, G);
+    sync_all(P, G);
     grid_value(red, kSlotD2, G, &s_val[0]);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -759,13 +771,13 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     // stage 2 (+ observations of the previous accepted step)
     if (PF && P.x2) {
       x2_pass(P, c, s0, s1);
-      grid_barrier(P.bar, G);
+      sync_all(P, G);
       stage_pass<2, ST, true>(P, c, s0, s1, sval, soff, &ring);
     } else {
       stage_pass<2, ST == 2 ? 1 : ST>(P, c, s0, s1, sval, soff, &ring);
     }
     if (c.np) observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
-    grid_barrier(P.bar, G);
+    sync_all(P, G);
     if (c.np) {
       observe_commit(P, c, slots(c.obs_par), G);
       __syncthreads();
@@ -775,17 +787,17 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
       }
     }
     stage_pass<3, ST>(P, c, s0, s1, sval, soff, &ring);
-    grid_barrier(P.bar, G);
+    sync_all(P, G);
     stage_pass<4, ST>(P, c, s0, s1, sval, soff, &ring);
-    grid_barrier(P.bar, G);
+    sync_all(P, G);
     stage_pass<5, ST>(P, c, s0, s1, sval, soff, &ring);
-    grid_barrier(P.bar, G);
+    sync_all(P, G);
     stage_pass<6, ST>(P, c, s0, s1, sval, soff, &ring);
-    grid_barrier(P.bar, G);
+    sync_all(P, G);
     double esq = stage_pass<7, ST>(P, c, s0, s1, sval, soff, &ring);
     esq = block_sum(esq, s_red);
     if (threadIdx.x == 0) red[static_cast<long long>(kSlotErr) * G + rank] = esq;
-    grid_barrier(P.bar, G);
+    sync_all(P, G);
     grid_value(red, kSlotErr, G, &s_val[0]);
     __syncthreads();
     if (threadIdx.x == 0) finish_attempt(P, c, s_val[0], kcap);
@@ -835,10 +847,48 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
 }
 
 template <int MODE, int ST>
+cudaLaunchConfig_t cluster_cfg(int grid, size_t smem, cudaLaunchAttribute* at) {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(dp5_grid_kernel<MODE, ST>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = grid;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+template <int MODE, int ST>
 cudaError_t launch_one(const GridProblem& P, int grid, cudaStream_t s) {
+  if (P.cluster) {  // the whole grid as one cluster: co-scheduled by construction
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t cfg = cluster_cfg<MODE, ST>(grid, grid_smem_bytes(P, ST), at);
+    cfg.stream = s;
+    return cudaLaunchKernelEx(&cfg, dp5_grid_kernel<MODE, ST>, P);
+  }
   void* args[] = {const_cast<GridProblem*>(&P)};
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dp5_grid_kernel<MODE, ST>), dim3(grid),
                                      dim3(kThreads), args, grid_smem_bytes(P, ST), s);
+}
+
+template <int MODE, int ST>
+int max_cluster_one(size_t smem) {
+  for (int c = 16; c >= 2; c /= 2) {
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t cfg = cluster_cfg<MODE, ST>(c, smem, at);
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, dp5_grid_kernel<MODE, ST>, &cfg) == cudaSuccess && nc > 0) return c;
+    cudaGetLastError();
+  }
+  return 0;
 }
 
 template <int MODE, int ST>
@@ -868,6 +918,12 @@ int grid_max_blocks_per_sm(int mode, int st, size_t dyn_smem) {
   if (mode == 0)
     return st == 2 ? occupancy_one<0, 2>(dyn_smem) : st == 1 ? occupancy_one<0, 1>(dyn_smem) : occupancy_one<0, 0>(dyn_smem);
   return st == 2 ? occupancy_one<1, 2>(dyn_smem) : st == 1 ? occupancy_one<1, 1>(dyn_smem) : occupancy_one<1, 0>(dyn_smem);
+}
+
+int grid_max_cluster(int mode, int st, size_t dyn_smem) {
+  if (mode == 0)
+    return st == 2 ? max_cluster_one<0, 2>(dyn_smem) : st == 1 ? max_cluster_one<0, 1>(dyn_smem) : max_cluster_one<0, 0>(dyn_smem);
+  return st == 2 ? max_cluster_one<1, 2>(dyn_smem) : st == 1 ? max_cluster_one<1, 1>(dyn_smem) : max_cluster_one<1, 0>(dyn_smem);
 }
 
 cudaError_t launch_grid_dp5(const GridProblem& P, int mode, int st, int grid, cudaStream_t s) {

@@ -20,6 +20,7 @@ struct GridCtl {
 };
 
 struct GridProblem {
+  int cluster;    // 1: the whole grid is one thread-block cluster (hardware cluster barriers)
   int smem_dict;  // > 0: the single-term coded generator's dictionary (entries) staged in shared memory
   int x2;         // materialise the stage-2 input (one extra pass + barrier, half the stage-2 gathers)
   int n;     // vector length (d*d for mesolve, d for sesolve)
@@ -57,5 +58,7 @@ int grid_threads();
 size_t grid_smem_bytes(const GridProblem& P, int st);
 int grid_max_blocks_per_sm(int mode, int st, size_t dyn_smem = 0);
 cudaError_t launch_grid_dp5(const GridProblem& P, int mode, int st, int grid, cudaStream_t s);
+// largest grid that runs as ONE thread-block cluster (<= 16 CTAs, one per SM), 0 if none
+int grid_max_cluster(int mode, int st, size_t dyn_smem);
 
 }  // namespace qsg

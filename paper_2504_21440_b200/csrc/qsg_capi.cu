@@ -809,6 +809,26 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   int grid = static_cast<int>(std::min<long long>(max_grid, std::max<long long>(1, (nblk + 3) / 4)));
   if (const char* eg = std::getenv("QSG_GRID")) grid = std::max(1, std::min(max_grid, std::atoi(eg)));
   grid = static_cast<int>(std::min<long long>(grid, nblk));
+  // Small systems (scripts/probe_small_grid.py, profiles/r02_small_grid.log, Kerr mesolve us per
+  // DP5 attempt): every cross-CTA barrier also invalidates L1, so the operator and the state come
+  // back from L2 each pass.
+  //  * <= 16 slices (Kerr N = 20, 400 rows): ONE CTA, no grid barrier at all: 14.5 us against
+  //    23.4 us on 4 CTAs;
+  //  * <= 96 slices (Kerr N = 50, 2,500 rows): one 16-CTA thread-block cluster, hardware cluster
+  //    barrier: 18.6 us against 22.8 us on a 20-CTA cooperative grid;
+  //  * larger (N >= 100): the cooperative grid (N = 100: 21.6 us on 79 CTAs vs 29.5 us as a cluster).
+  // QSG_GRID_CLUSTER=1/0 forces/disables the cluster; QSG_GRID still sets the CTA count.
+  if (!std::getenv("QSG_GRID") && nblk <= 16) grid = 1;
+  {
+    const char* gc = std::getenv("QSG_GRID_CLUSTER");
+    const bool want = gc ? gc[0] == '1' : (nblk > 16 && nblk <= 96 && !std::getenv("QSG_GRID"));
+    const int cmax = want ? grid_max_cluster(mode, st, dyn) : 0;
+    if (cmax > 0) {
+      P.cluster = 1;
+      grid = static_cast<int>(std::min<long long>(cmax, nblk));
+      if (const char* cs = std::getenv("QSG_GRID_CLUSTER_SIZE")) grid = std::max(1, std::min(grid, std::atoi(cs)));
+    }
+  }
   (void)threads;
   if ((ce = d_ctl.alloc(sizeof(GridCtl), s)) || (ce = d_red.alloc(sizeof(double) * kNumSlots * grid, s)) ||
       (ce = d_bar.alloc(2 * sizeof(unsigned), s)))
