@@ -170,3 +170,21 @@ def test_coupled_kerr_sweep_points_match_oracle(ctx):
         ex, st, _ = m.mesolve(t, params=prm)
         assert normwise_rel(res["expect"][p], ex) <= 1e-6, p
         assert_stats_close(res["stats"][p], st)
+
+
+def test_tfim10_key_aligned_solve(ctx, tfim10, monkeypatch):
+    """The opt-in key-aligned store (QSG_KA_STORE / QSG_KA_SOLVE, TMA ring) on the full configs[1]
+    solve: same golden, same step statistics as the default coded path."""
+    m, _, eops, rho0 = tfim10
+    H = m.export(q.SEL_H_CONST)
+    cops = [m.export(q.SEL_C_OP, k) for k in range(m.n_cops)]
+    ref, st, t = golden("tfim10")
+    monkeypatch.setenv("QSG_KA_SOLVE", "1")
+    op = ctx.liouvillian(H, cops)
+    info = q.op_store_info(op)
+    assert info["store"] == "key-aligned" and 0 < info["ka_bytes"] < info["coded_bytes"]
+    dev = q.mesolve(ctx, q.Generator([op]), m.dim, rho0, t, eops)
+    op.close()
+    assert dev["store"] == 2
+    assert normwise_rel(dev["expect"], ref) <= 1e-6
+    assert_stats_close(dev["stats"], st)
