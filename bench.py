@@ -394,6 +394,10 @@ def kerr_cutoff_mesolve(ctx, q, peak, cpu=False):
     at every N, reported per DP5 attempt beside the device's per-attempt time."""
     out = {}
     tl = np.linspace(0.0, 10.0, 101)
+    kerr_traffic = {}
+    tp = os.path.join(ROOT, "profiles", "r02_kerr_cutoff_traffic.json")
+    if os.path.exists(tp):
+        kerr_traffic = json.load(open(tp)).get("cutoffs", {})
     for N in KERR_CUTOFFS:
         m = q.Model("kerr", N, 1.0, 0.01, 2.0, 1.0)
         Lk = m.export(q.SEL_L_CONST)
@@ -409,6 +413,10 @@ def kerr_cutoff_mesolve(ctx, q, peak, cpu=False):
         out[f"N{N}"] = {"rows": n, "nnz": nnz, "solve_ms": r["kernel_ms"], "attempts": r["attempts"],
                         "us_per_attempt": r["kernel_ms"] * 1e3 / r["attempts"], "GBps_model": b / r["kernel_ms"] / 1e6,
                         "grid_ctas": r["grid_ctas"], "note": "L2-resident operator: GB/s can exceed the HBM rate"}
+        tr = kerr_traffic.get(f"N{N}")
+        if tr:  # committed ncu capture of the same solve (profiles/r02_kerr_cutoff_traffic.json)
+            out[f"N{N}"]["ncu"] = {"dram_bytes": tr["dram_bytes"], "lts_bytes": tr["lts_bytes"],
+                                   "lts_GBps": tr["lts_GBps"], "gpu_time_ms": tr["gpu_time_ms"]}
         if cpu:
             from oracle import oracle as O
             O.set_threads(1)

@@ -281,6 +281,9 @@ __device__ __forceinline__ double2 sell_row_slot(const DevSell& A, int row, XF&&
   return acc;
 }
 
+// Inlined at each of the 9 call sites: an out-of-line copy per gather source (lambda captures
+// through the stack, ABI register saves) measured 595 / 508 traj/s against 785 / 767 (TFIM-14,
+// 2,368 trajectories, key-aligned / plain rows; profiles/r02_batch_noinline_ab.log).
 template <bool KA = false, class XF>
 __device__ __forceinline__ double2 gen_row_slot(const DevGen& g, const double* params, int row, double t,
                                                 XF&& xf) {
