@@ -14,6 +14,7 @@
 // keeps the kernel at <= 64 registers and 2 CTAs x 16 warps per SM for latency hiding.
 //
 // Passes per attempt: 6 (stage 2 gathers y + h*a21*k1 on the fly), one grid barrier each.
+#include <algorithm>
 #include <cstdio>
 
 #include "engine.cuh"
@@ -578,15 +579,29 @@ __device__ void begin_attempt(const GridProblem& P, Ctl& c) {
 }
 
 // thread 0: accept / reject (integrator.hpp:116-145) and event bookkeeping (evolve.cpp:160-165)
-__device__ void finish_attempt(const GridProblem& P, Ctl& c, double err_sq, int kcap) {
+// err of the attempt from the summed squares (integrator.hpp:116-117)
+__device__ __forceinline__ double attempt_err(const GridProblem& P, double err_sq) {
+  const double err = sqrt(err_sq / static_cast<double>(P.n));
+  return isfinite(err) ? err : 10.0;
+}
+
+// The controller's two powers pow(err, expo1) and pow(facold, beta) (integrator.hpp:120-121,144),
+// evaluated by lanes 0 and 1 of the calling warp at once; every lane gets both.
+__device__ __forceinline__ double2 controller_pows(double err, double facold) {
+  const int lane = threadIdx.x & 31;
+  const double v = pow(lane == 0 ? err : facold, lane == 0 ? dp::expo1 : dp::beta);
+  return make_double2(__shfl_sync(0xffffffffu, v, 0), __shfl_sync(0xffffffffu, v, 1));
+}
+
+// pw: {pow(err, expo1), pow(facold, beta)} precomputed (controller_pows), or nullptr
+__device__ void finish_attempt(const GridProblem& P, Ctl& c, double err_sq, int kcap, const double2* pw = nullptr) {
   using namespace dp;
-  double err = sqrt(err_sq / static_cast<double>(P.n));
-  if (!isfinite(err)) err = 10.0;
+  const double err = attempt_err(P, err_sq);
   c.rhs_evals += 6;
   ++c.attempts_total;
   if (err <= 1.0) {
-    const double fac11 = pow(err, expo1);
-    double fac = fac11 / pow(c.facold, beta);
+    const double fac11 = pw ? pw->x : pow(err, expo1);
+    double fac = fac11 / (pw ? pw->y : pow(c.facold, beta));
     fac = fmax(facc2, fmin(facc1, fac / safe));
     const double h_new = c.hh / fac;
     c.facold = fmax(err, 1e-4);
@@ -611,7 +626,7 @@ __device__ void finish_attempt(const GridProblem& P, Ctl& c, double err_sq, int 
     c.done = last || c.next >= P.n_ev;
   } else {
     ++c.rejected;
-    c.h = c.hh / fmin(facc1, pow(err, expo1) / safe);
+    c.h = c.hh / fmin(facc1, (pw ? pw->x : pow(err, expo1)) / safe);
     c.flush = 0;
     c.done = 0;
   }
@@ -800,7 +815,10 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     sync_all(P, G);
     grid_value(red, kSlotErr, G, &s_val[0]);
     __syncthreads();
-    if (threadIdx.x == 0) finish_attempt(P, c, s_val[0], kcap);
+    if (threadIdx.x < 32) {
+      const double2 pw = controller_pows(attempt_err(P, s_val[0]), c.facold);
+      if (threadIdx.x == 0) finish_attempt(P, c, s_val[0], kcap, &pw);
+    }
     __syncthreads();
     while (c.flush) {  // pending list full, or the solve ends with events pending
       flush_obs();
@@ -844,6 +862,536 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     o->attempts = c.attempts_total;
     o->final_buf = 0;
   }
+}
+
+// =================================================================================================
+// K-cluster: the whole solve resident in the distributed shared memory of ONE thread-block cluster
+// (small systems, configs[0]/[3]). CTA r owns rows [r*R, (r+1)*R) (R a multiple of 32): its slices
+// of the operator (column pre-split into (owner CTA, local row), values) and its rows of the 11
+// state vectors live in its shared memory for the whole solve. The SpMV gathers x[col] from the
+// owner's shared memory (ld.shared::cluster), the epilogue touches only local rows, and the passes
+// are separated by hardware cluster barriers. Nothing is read from L2 after the prologue, so no
+// barrier's L1 invalidation matters. Control, events and the PI controller are the grid engine's
+// (Ctl, begin_attempt, finish_attempt), replicated identically in every CTA; reductions are CTA
+// partials read by every CTA from every CTA's shared memory in rank order (deterministic).
+constexpr int kClThreads = 512;
+
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cl_map(unsigned saddr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double2 cl_ld2(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ double cl_ld(unsigned a) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+
+// element c (global index) of logical buffer b, from its owner CTA
+__device__ __forceinline__ double2 cl_elem(double2* const* p, int b, int c, int R) {
+  const unsigned owner = static_cast<unsigned>(c / R);
+  const unsigned loc = static_cast<unsigned>(c - static_cast<int>(owner) * R);
+  return cl_ld2(cl_map(smem_u32(p[b] + loc), owner));
+}
+// dense output (integrator.hpp:127-131,150-154) at global index c, read from its owner CTA
+__device__ __forceinline__ double2 cl_dense(double2* const* p, int c, double theta, double h, int R) {
+  if (isnan(theta)) return cl_elem(p, Y, c, R);
+  const double2 yo = cl_elem(p, YO, c, R), y1 = cl_elem(p, Y, c, R), k1 = cl_elem(p, K7, c, R),
+                k7 = cl_elem(p, K1, c, R), k3 = cl_elem(p, K3, c, R), k4 = cl_elem(p, K4, c, R),
+                k5 = cl_elem(p, K5, c, R), k6 = cl_elem(p, K6, c, R);
+  using namespace dp;
+  const double th1 = 1.0 - theta;
+  const double2 rc2 = csub(y1, yo);
+  const double2 rc3 = csub(cscale(h, k1), rc2);
+  const double2 rc4 = csub(csub(rc2, cscale(h, k7)), rc3);
+  double2 rc5;
+  rc5.x = h * (d1 * k1.x + d3 * k3.x + d4 * k4.x + d5 * k5.x + d6 * k6.x + d7 * k7.x);
+  rc5.y = h * (d1 * k1.y + d3 * k3.y + d4 * k4.y + d5 * k5.y + d6 * k6.y + d7 * k7.y);
+  double2 o;
+  o.x = yo.x + theta * (rc2.x + th1 * (rc3.x + theta * (rc4.x + th1 * rc5.x)));
+  o.y = yo.y + theta * (rc2.y + th1 * (rc3.y + theta * (rc4.y + th1 * rc5.y)));
+  return o;
+}
+
+// Cluster-wide deterministic sum of one value per CTA: every CTA writes its partial into slot k of
+// its own reduction array; after the caller's cluster barrier a whole warp reads slot k of the C
+// CTAs (lane r from CTA r, all loads in flight at once) and folds them in a fixed xor tree, the
+// same order in every CTA. Returns the total in every lane.
+__device__ __forceinline__ double cl_warp_sum(double* red, int k, int C) {
+  const int lane = threadIdx.x & 31;
+  double v = lane < C ? cl_ld(cl_map(smem_u32(red + k), static_cast<unsigned>(lane))) : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One SpMV row of the CTA's resident operator slice sl (lane = row in slice), gathering logical
+// buffer xb (S2: y + h a21 k1 on the fly) from every CTA's shared memory.
+template <bool S2>
+__device__ __forceinline__ double2 cl_row(const int* rowlen, const int* soff, const unsigned* tgt, const double2* val,
+                                          int sl, int lane, double2* const* p, int xb, double hh) {
+  const int len = rowlen[sl * 32 + lane];
+  const int base = soff[sl] * 32 + lane;
+  const unsigned xa = smem_u32(p[xb]);
+  const unsigned ya = smem_u32(p[Y]), ka = smem_u32(p[K1]);
+  double2 acc = make_double2(0.0, 0.0);
+  for (int j = 0; j < len; j += 4) {
+    unsigned tg[4];
+    double2 v[4], x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      tg[u] = j + u < len ? tgt[base + 32 * (j + u)] : 0u;
+      v[u] = j + u < len ? val[base + 32 * (j + u)] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (j + u < len) {
+        const unsigned own = tg[u] >> 24, off = (tg[u] & 0xffffffu) * 16u;
+        if constexpr (S2) {
+          const double2 a = cl_ld2(cl_map(ya + off, own)), q = cl_ld2(cl_map(ka + off, own));
+          x[u] = make_double2(a.x + hh * (dp::a21 * q.x), a.y + hh * (dp::a21 * q.y));
+        } else {
+          x[u] = cl_ld2(cl_map(xa + off, own));
+        }
+      } else {
+        x[u] = make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (j + u < len) cfma(v[u], x[u], acc);
+  }
+  return acc;
+}
+
+#ifdef QSG_CL_TIMING
+__device__ unsigned long long g_cl_ns[16];
+__device__ __forceinline__ unsigned long long cl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CL_T(k)                                                  \
+  do {                                                           \
+    if (rank == 0 && threadIdx.x == 0) {                         \
+      const unsigned long long _t = cl_now();                    \
+      g_cl_ns[k] += _t - cl_t_last;                              \
+      cl_t_last = _t;                                            \
+    }                                                            \
+  } while (0)
+#else
+#define CL_T(k) \
+  do {          \
+  } while (0)
+#endif
+
+template <int MODE>
+__global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid_constant__ GridProblem P,
+                                                                      const ClLayout L) {
+  __shared__ double s_red[kClThreads / 32];
+  __shared__ Ctl c;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  const int C = gridDim.x;
+  const int rank = static_cast<int>(cl_rank());
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = kClThreads / 32;
+  const int n = P.n, R = L.R;
+  const int r0 = rank * R, r1 = min(n, r0 + R);
+  const int nsl = (max(0, r1 - r0) + 31) >> 5;  // this CTA's slices
+  double2* vec = reinterpret_cast<double2*>(s_dyn + L.vec);
+  int* rowlen = reinterpret_cast<int*>(s_dyn + L.rowlen);
+  int* soff = reinterpret_cast<int*>(s_dyn + L.soff);
+  unsigned* tgt = reinterpret_cast<unsigned*>(s_dyn + L.tgt);
+  double2* val = reinterpret_cast<double2*>(s_dyn + L.val);
+  double* red = reinterpret_cast<double*>(s_dyn + L.red);  // [0..3] control sums, [4..] observations
+  const int kcap = max(1, min(kMaxPending, kObsSlots / (2 * max(1, P.n_e))));
+
+  // ---- prologue: the CTA's operator slices into shared memory (columns pre-split by owner) and
+  // y0 rows; every other buffer starts uninitialised like the grid engine's
+  const DevSell& A = P.gen.A[0];
+  for (int i = threadIdx.x; i < L.S * 32; i += kClThreads) {
+    const int sl = i >> 5, row = r0 + i;
+    rowlen[i] = row < n ? __ldg(A.rowlen + row) : 0;
+    if ((i & 31) == 0) soff[sl] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // local slice offsets (in 32-entry columns), the global SELL widths
+    int acc = 0;
+    for (int sl = 0; sl < L.S; ++sl) {
+      soff[sl] = acc;
+      const int gs = (r0 >> 5) + sl;
+      acc += (r0 + sl * 32 < n) ? static_cast<int>(__ldg(A.slice_off + gs + 1) - __ldg(A.slice_off + gs)) : 0;
+    }
+    soff[L.S] = acc;
+  }
+  __syncthreads();
+  for (int sl = warp; sl < nsl; sl += W) {
+    const int gs = (r0 >> 5) + sl;
+    const long long gbase = __ldg(A.slice_off + gs) * 32;
+    const int wd = soff[sl + 1] - soff[sl];
+    for (int j = 0; j < wd; ++j) {
+      const long long gi = gbase + 32LL * j + lane;
+      const int col = __ldg(A.col + gi);
+      const int own = col / R;
+      tgt[(soff[sl] + j) * 32 + lane] = (static_cast<unsigned>(own) << 24) | static_cast<unsigned>(col - own * R);
+      val[(soff[sl] + j) * 32 + lane] = __ldg(A.val + gi);
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 11; ++i) c.p[i] = vec + static_cast<long long>(i) * R;
+    c.t = c.t_old = P.t0;
+    c.h = c.h_last = 0.0;
+    c.facold = 1e-4;
+    c.steps = c.rejected = c.rhs_evals = c.attempts_total = 0;
+    c.status = kRunning;
+    c.attempts = c.next = c.np = c.obs_par = c.flush = c.done = 0;
+    c.fail_t = 0.0;
+    while (c.next < P.n_ev && P.ev_t[c.next] <= P.t0 + P.eps_t && c.np < kcap)
+      push_pending(P, c, __longlong_as_double(0x7ff8000000000000ll));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < r1 - r0; i += kClThreads) c.p[Y][i] = P.buf[0][r0 + i];  // y0 (host-staged)
+  cl_sync();
+
+  // ---- observation pass: pending events -> expectation partials in red[4 + 2*(q*n_e+e)] and saves
+  // bank of observation slots in red[] (double-buffered by c.obs_par, like the grid engine's):
+  // a bank is rewritten two observation events later, after at least one more cluster barrier
+  auto obs_bank = [&](int par) { return red + 4 + par * kObsSlots; };
+  auto observe = [&]() {
+    double2* const* p = c.p;
+    const int np = c.np;
+    const double hl = c.h_last;
+    const int gt = rank * kClThreads + threadIdx.x, gs = C * kClThreads;
+    double* bank = obs_bank(c.obs_par);
+    const int npairs = np * P.n_e;
+    constexpr int kV = 8;  // (event, e_op) pairs reduced together
+    for (int b0 = 0; b0 < npairs; b0 += kV) {
+      double2 acc[kV];
+#pragma unroll
+      for (int v = 0; v < kV; ++v) acc[v] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int v = 0; v < kV; ++v) {
+        const int pr = b0 + v;
+        if (pr >= npairs) break;
+        const int q = pr / P.n_e, e = pr % P.n_e;
+        const double th = c.pend[q].theta;
+        if (c.pend[q].grid_idx < 0) continue;
+        if (MODE == 0) {
+          for (int k = P.eo_off[e] + gt; k < P.eo_off[e + 1]; k += gs) {
+            const int i = P.eo_i[k], j = P.eo_j[k];
+            const double2 rji = cl_dense(p, i * P.d + j, th, hl, R), rij = cl_dense(p, j * P.d + i, th, hl, R);
+            acc[v] = cadd(acc[v], cmul(P.eo_v[k], cscale(0.5, cadd(rji, cconj(rij)))));
+          }
+        } else {
+          const int* rp = P.se_rowptr + static_cast<long long>(e) * (P.n + 1);
+          const long long off = P.se_off[e];
+          for (int r = r0 + threadIdx.x; r < r1; r += kClThreads) {
+            double2 ev = make_double2(0.0, 0.0);
+            for (int k = rp[r]; k < rp[r + 1]; ++k)
+              ev = cadd(ev, cmul(P.se_val[off + k], cl_dense(p, P.se_col[off + k], th, hl, R)));
+            acc[v] = cadd(acc[v], cmul(cconj(cl_dense(p, r, th, hl, R)), ev));
+          }
+        }
+      }
+      // one block reduction for all 2 kV values: warp shuffles, one smem row per warp, warp 0
+      // folds the warps in order (the same order in every CTA)
+      __shared__ double s_obs[kClThreads / 32][2 * kV];
+#pragma unroll
+      for (int v = 0; v < kV; ++v) {
+        const double x = warp_sum(acc[v].x), y = warp_sum(acc[v].y);
+        if (lane == 0) {
+          s_obs[warp][2 * v] = x;
+          s_obs[warp][2 * v + 1] = y;
+        }
+      }
+      __syncthreads();
+      if (warp == 0 && lane < 2 * kV && b0 + lane / 2 < npairs) {
+        double t = 0.0;
+        for (int w = 0; w < W; ++w) t += s_obs[w][lane];
+        bank[2 * b0 + lane] = t;
+      }
+      __syncthreads();
+    }
+    for (int q = 0; q < np; ++q) {
+      if (c.pend[q].save_idx < 0) continue;
+      const double th = c.pend[q].theta;
+      double2* out = P.states + static_cast<long long>(c.pend[q].save_idx) * P.n;
+      for (int r = r0 + threadIdx.x; r < r1; r += kClThreads) {
+        if (MODE == 0) {
+          const int i = r % P.d, j = r / P.d;
+          out[r] = cscale(0.5, cadd(cl_dense(p, r, th, hl, R), cconj(cl_dense(p, i * P.d + j, th, hl, R))));
+        } else {
+          out[r] = cl_dense(p, r, th, hl, R);
+        }
+      }
+    }
+  };
+  // after the barrier that follows observe(): every CTA folds the partials; CTA 0 writes expect[]
+  auto observe_commit_cl = [&]() {
+    const int nv = 2 * c.np * P.n_e;
+    const int base = static_cast<int>(obs_bank(c.obs_par) - red);
+    if (rank == 0)
+      for (int s2 = warp; s2 < nv; s2 += W) {  // one warp per value: the C partials in flight at once
+        const double v = cl_warp_sum(red, base + s2, C);
+        const int q = (s2 / 2) / P.n_e, e = (s2 / 2) % P.n_e;
+        if (lane == 0 && c.pend[q].grid_idx >= 0)
+          reinterpret_cast<double*>(P.expect + static_cast<long long>(c.pend[q].grid_idx) * P.n_e + e)[s2 & 1] = v;
+      }
+  };
+  auto flush = [&]() {
+    observe();
+    cl_sync();
+    observe_commit_cl();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      c.np = 0;
+      c.obs_par ^= 1;
+    }
+    __syncthreads();
+  };
+
+  // ---- start + initial_step (integrator.hpp:61-69,157-187)
+  {
+    double a0 = 0.0, a1 = 0.0;
+    for (int sl = warp; sl < nsl; sl += W) {
+      const int lr = sl * 32 + lane;
+      const double2 k = cl_row<false>(rowlen, soff, tgt, val, sl, lane, c.p, Y, 0.0);
+      if (r0 + lr < r1) {
+        c.p[K1][lr] = k;
+        const double2 yy = c.p[Y][lr];
+        const double sc = P.atol + P.rtol * cabs_(yy);
+        a0 += cnorm(make_double2(yy.x / sc, yy.y / sc));
+        a1 += cnorm(make_double2(k.x / sc, k.y / sc));
+      }
+    }
+    a0 = block_sum(a0, s_red);
+    a1 = block_sum(a1, s_red);
+    if (threadIdx.x == 0) {
+      red[0] = a0;
+      red[1] = a1;
+    }
+    if (c.np) observe();
+    cl_sync();
+    if (c.np) observe_commit_cl();
+    __shared__ double s_tot[3];
+    if (warp == 0) {
+      const double t0 = cl_warp_sum(red, 0, C), t1 = cl_warp_sum(red, 1, C);
+      if (lane == 0) {
+        s_tot[0] = t0;
+        s_tot[1] = t1;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double dd0 = sqrt(s_tot[0] / static_cast<double>(n));
+      const double dd1 = sqrt(s_tot[1] / static_cast<double>(n));
+      if (c.np) c.obs_par ^= 1;
+      c.np = 0;
+      c.rhs_evals += 1;
+      double h0 = (dd0 < 1e-5 || dd1 < 1e-5) ? 1e-6 : 0.01 * dd0 / dd1;
+      h0 = fmin(h0, P.tf - c.t);
+      if (!(h0 > 0)) h0 = 1e-6;
+      c.h0 = h0;
+      c.d1 = dd1;
+    }
+    cl_sync();  // red[0..1] and the observation slots are read before anyone rewrites them
+    double a2 = 0.0;
+    {
+      const double h0 = c.h0;
+      for (int sl = warp; sl < nsl; sl += W) {  // SB = y + h0 k1, then G(t0 + h0) SB
+        const int lr = sl * 32 + lane;
+        if (r0 + lr < r1) {
+          const double2 u = c.p[Y][lr], v = c.p[K1][lr];
+          c.p[SB][lr] = make_double2(u.x + h0 * v.x, u.y + h0 * v.y);
+        }
+      }
+      cl_sync();
+      for (int sl = warp; sl < nsl; sl += W) {
+        const int lr = sl * 32 + lane;
+        const double2 k = cl_row<false>(rowlen, soff, tgt, val, sl, lane, c.p, SB, 0.0);
+        if (r0 + lr < r1) {
+          const double2 yy = c.p[Y][lr], kk1 = c.p[K1][lr];
+          const double sc = P.atol + P.rtol * cabs_(yy);
+          const double2 df = csub(k, kk1);
+          a2 += cnorm(make_double2(df.x / sc, df.y / sc));
+        }
+      }
+    }
+    a2 = block_sum(a2, s_red);
+    if (threadIdx.x == 0) red[2] = a2;
+    cl_sync();
+    if (warp == 0) {
+      const double t2 = cl_warp_sum(red, 2, C);
+      if (lane == 0) s_tot[2] = t2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      c.rhs_evals += 1;
+      const double dd2 = sqrt(s_tot[2] / static_cast<double>(n)) / c.h0;
+      double h1;
+      if (fmax(c.d1, dd2) <= 1e-15) h1 = fmax(1e-6, c.h0 * 1e-3);
+      else h1 = pow(0.01 / fmax(c.d1, dd2), 0.2);
+      c.h = fmin(fmin(100.0 * c.h0, h1), P.tf - c.t);
+    }
+    __syncthreads();
+  }
+
+  // ---- solve loop (evolve.cpp:156-167)
+  using namespace dp;
+#ifdef QSG_CL_TIMING
+  unsigned long long cl_t_last = 0;
+  if (rank == 0 && threadIdx.x == 0) cl_t_last = cl_now();
+#endif
+  for (;;) {
+    if (threadIdx.x == 0) {
+      if (c.next >= P.n_ev) c.done = 1;
+      else begin_attempt(P, c);
+    }
+    __syncthreads();
+    CL_T(0);
+    if (c.done || c.status != kRunning) break;
+    const double hh = c.hh, t = c.t;
+    (void)t;
+    // stage passes 2..7 (integrator.hpp:91-102) on local rows, gathers from the cluster
+    for (int S = 2; S <= 7; ++S) {
+      const int xb = S == 2 ? Y : (S == 3 || S == 5 || S == 7) ? SA : SB;
+      const int ko = S == 2 ? K2 : S == 3 ? K3 : S == 4 ? K4 : S == 5 ? K5 : S == 6 ? K6 : K7;
+      const int xo = (S == 3 || S == 5) ? SB : SA;
+      double esq = 0.0;
+      double2* const* p = c.p;
+      for (int sl = warp; sl < nsl; sl += W) {
+        const int lr = sl * 32 + lane;
+        const double2 k = S == 2 ? cl_row<true>(rowlen, soff, tgt, val, sl, lane, p, Y, hh)
+                                 : cl_row<false>(rowlen, soff, tgt, val, sl, lane, p, xb, hh);
+        if (r0 + lr >= r1) continue;
+        const double2 yy = p[Y][lr], q1 = p[K1][lr];
+        p[ko][lr] = k;
+        if (S == 2) {
+          p[xo][lr] = make_double2(yy.x + hh * (a31 * q1.x + a32 * k.x), yy.y + hh * (a31 * q1.y + a32 * k.y));
+        } else if (S == 3) {
+          const double2 q2 = p[K2][lr];
+          p[xo][lr] = make_double2(yy.x + hh * (a41 * q1.x + a42 * q2.x + a43 * k.x),
+                                   yy.y + hh * (a41 * q1.y + a42 * q2.y + a43 * k.y));
+        } else if (S == 4) {
+          const double2 q2 = p[K2][lr], q3 = p[K3][lr];
+          p[xo][lr] = make_double2(yy.x + hh * (a51 * q1.x + a52 * q2.x + a53 * q3.x + a54 * k.x),
+                                   yy.y + hh * (a51 * q1.y + a52 * q2.y + a53 * q3.y + a54 * k.y));
+        } else if (S == 5) {
+          const double2 q2 = p[K2][lr], q3 = p[K3][lr], q4 = p[K4][lr];
+          p[xo][lr] = make_double2(yy.x + hh * (a61 * q1.x + a62 * q2.x + a63 * q3.x + a64 * q4.x + a65 * k.x),
+                                   yy.y + hh * (a61 * q1.y + a62 * q2.y + a63 * q3.y + a64 * q4.y + a65 * k.y));
+        } else if (S == 6) {
+          const double2 q3 = p[K3][lr], q4 = p[K4][lr], q5 = p[K5][lr];
+          p[xo][lr] = make_double2(yy.x + hh * (a71 * q1.x + a73 * q3.x + a74 * q4.x + a75 * q5.x + a76 * k.x),
+                                   yy.y + hh * (a71 * q1.y + a73 * q3.y + a74 * q4.y + a75 * q5.y + a76 * k.y));
+        } else {
+          const double2 q3 = p[K3][lr], q4 = p[K4][lr], q5 = p[K5][lr], q6 = p[K6][lr], y1 = p[SA][lr];
+          double2 e;
+          e.x = hh * (e1 * q1.x + e3 * q3.x + e4 * q4.x + e5 * q5.x + e6 * q6.x + e7 * k.x);
+          e.y = hh * (e1 * q1.y + e3 * q3.y + e4 * q4.y + e5 * q5.y + e6 * q6.y + e7 * k.y);
+          const double sc = P.atol + P.rtol * fmax(cabs_(yy), cabs_(y1));
+          const double qq = cabs_(e) / sc;
+          esq += qq * qq;
+        }
+      }
+      CL_T(1);
+      if (S == 2 && c.np) observe();  // the previous step's events, on the buffers of that step
+      CL_T(2);
+      if (S == 7) {
+        esq = block_sum(esq, s_red);
+        if (threadIdx.x == 0) red[3] = esq;
+      }
+      cl_sync();
+      CL_T(3);
+      if (S == 2 && c.np) {
+        observe_commit_cl();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          c.np = 0;
+          c.obs_par ^= 1;
+        }
+        __syncthreads();
+      }
+      CL_T(4);
+    }
+    if (warp == 0) {
+      const double e2 = cl_warp_sum(red, 3, C);
+      const double2 pw = controller_pows(attempt_err(P, e2), c.facold);
+      if (lane == 0) finish_attempt(P, c, e2, kcap, &pw);
+    }
+    __syncthreads();
+    CL_T(5);
+    while (c.flush) {
+      flush();
+      if (threadIdx.x == 0) {
+        while (c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t && c.np < kcap)
+          push_pending(P, c, (fmin(P.ev_t[c.next], c.t) - c.t_old) / c.h_last);
+        const bool more = c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t;
+        c.flush = more || (c.t >= P.tf - P.eps_t && c.np > 0);
+      }
+      __syncthreads();
+    }
+    CL_T(6);
+    // red[3] is read by every CTA (finish_attempt above) before the next stage 7 rewrites it:
+    // the six stage barriers in between order that
+    if (c.done) break;
+  }
+  if (c.status == kRunning) {
+    if (c.np) flush();
+    while (c.next < P.n_ev) {
+      if (threadIdx.x == 0)
+        while (c.next < P.n_ev && c.np < kcap) push_pending(P, c, __longlong_as_double(0x7ff8000000000000ll));
+      __syncthreads();
+      flush();
+    }
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    GridCtl* o = P.ctl;
+    o->t = c.t;
+    o->h = c.h;
+    o->status = c.status == kRunning ? kDone : c.status;
+    o->fail_t = c.fail_t;
+    o->steps = c.steps;
+    o->rejected = c.rejected;
+    o->rhs_evals = c.rhs_evals;
+    o->attempts = c.attempts_total;
+    o->final_buf = 0;
+  }
+  cl_sync();  // no CTA leaves while another may still read its shared memory
+}
+
+template <int MODE>
+cudaError_t launch_cluster_one(const GridProblem& P, const ClLayout& L, int C, cudaStream_t s) {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(dp5_cluster_kernel<MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) ||
+      (e = cudaFuncSetAttribute(dp5_cluster_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(L.bytes))))
+    return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kClThreads);
+  cfg.dynamicSmemBytes = L.bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, dp5_cluster_kernel<MODE>, P, L);
 }
 
 template <int MODE, int ST>
@@ -926,6 +1474,61 @@ int grid_max_cluster(int mode, int st, size_t dyn_smem) {
   return st == 2 ? max_cluster_one<1, 2>(dyn_smem) : st == 1 ? max_cluster_one<1, 1>(dyn_smem) : max_cluster_one<1, 0>(dyn_smem);
 }
 
+// Plans the cluster-resident layout for a single-term plain-store generator: C CTAs of R rows
+// each (R a multiple of 32), all state and operator slices in shared memory. Returns false when
+// the system does not fit one 16-CTA cluster.
+bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, int n_obs_slots, int* C_out,
+                        ClLayout* plan) {
+  if (P.gen.n_terms != 1 || P.gen.A[0].code_bytes != 0) return false;
+  const int n = P.n;
+  const long long nsl = (n + 31) / 32;
+  // as many CTAs as there are slices, up to 16 (one cluster): each CTA's rows are a pass's
+  // latency-bound share of work, so the widest cluster is the fastest (profiles/r02_cluster_solve.log)
+  const int C0 = static_cast<int>(std::min<long long>(16, nsl));
+  for (int C = C0; C >= 2; C = C == C0 ? C0 : C) {
+    const int S = static_cast<int>((nsl + C - 1) / C);
+    const int R = 32 * S;
+    long long E = 0;  // entry capacity: widest CTA
+    for (int r = 0; r < C; ++r) {
+      const long long a = std::min<long long>(nsl, static_cast<long long>(r) * S), b = std::min<long long>(nsl, a + S);
+      E = std::max(E, 32 * (slice_off_host[b] - slice_off_host[a]));
+    }
+    auto al = [](unsigned x) { return (x + 15u) & ~15u; };
+    ClLayout L{};
+    L.R = R;
+    L.S = S;
+    L.E = static_cast<int>(E);
+    unsigned o = 0;
+    L.vec = o;
+    o = al(o + 11u * R * 16u);
+    L.rowlen = o;
+    o = al(o + 4u * 32u * S);
+    L.soff = o;
+    o = al(o + 4u * (S + 1));
+    L.tgt = o;
+    o = al(o + 4u * static_cast<unsigned>(E));
+    L.val = o;
+    o = al(o + 16u * static_cast<unsigned>(E));
+    L.red = o;
+    o = al(o + 8u * (4 + 2 * n_obs_slots));  // control sums + two observation banks
+    L.bytes = o;
+    const unsigned static_smem = sizeof(double) * (kClThreads / 32) + sizeof(Ctl);
+    // the smallest cluster whose per-CTA share fits (more CTAs only add DSMEM hops and barrier
+    // arrivals); 16 slices per CTA at most so every warp owns at most one slice per pass
+    if (L.bytes + static_smem <= 200u * 1024u && S <= 64 && R < (1 << 24)) {
+      *C_out = C;
+      *plan = L;
+      return true;
+    }
+    break;  // fewer CTAs only means more rows per CTA: it will not fit either
+  }
+  return false;
+}
+
+cudaError_t launch_cluster_dp5(const GridProblem& P, int mode, const ClLayout& L, int C, cudaStream_t s) {
+  return mode == 0 ? launch_cluster_one<0>(P, L, C, s) : launch_cluster_one<1>(P, L, C, s);
+}
+
 cudaError_t launch_grid_dp5(const GridProblem& P, int mode, int st, int grid, cudaStream_t s) {
   if (mode == 0)
     return st == 2 ? launch_one<0, 2>(P, grid, s) : st == 1 ? launch_one<0, 1>(P, grid, s) : launch_one<0, 0>(P, grid, s);
@@ -933,6 +1536,17 @@ cudaError_t launch_grid_dp5(const GridProblem& P, int mode, int st, int grid, cu
 }
 
 }  // namespace qsg
+
+#ifdef QSG_CL_TIMING
+extern "C" void qsg_debug_cluster_ns(unsigned long long* out16, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out16, qsg::g_cl_ns, sizeof(unsigned long long) * 16);
+  if (reset) {
+    static const unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(qsg::g_cl_ns, z, sizeof(z));
+  }
+}
+#endif
 
 #ifdef QSG_BAR_TIMING
 extern "C" void qsg_debug_barrier_ns(unsigned long long* wait_ns, unsigned long long* calls, int reset,

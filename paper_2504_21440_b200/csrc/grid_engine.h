@@ -53,6 +53,18 @@ struct GridProblem {
   unsigned* bar;     // grid barrier: one 64-bit arrival counter
 };
 
+// K-cluster (cluster-resident solve, grid_engine.cu): dynamic shared-memory layout of one CTA.
+struct ClLayout {
+  int R;  // rows per CTA (multiple of 32)
+  int S;  // slices per CTA = R / 32
+  int E;  // entry capacity (32 * the widest CTA's summed slice widths)
+  unsigned vec, rowlen, soff, tgt, val, red, bytes;
+};
+// true (and the cluster size / layout) when a single-term plain-store generator fits one cluster
+bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, int n_obs_slots, int* C_out,
+                        ClLayout* plan);
+cudaError_t launch_cluster_dp5(const GridProblem& P, int mode, const ClLayout& L, int C, cudaStream_t s);
+
 int grid_threads();
 // st: 0 generic rows, 1 dictionary-coded store (pipelined), 2 key-aligned store (TMA ring)
 size_t grid_smem_bytes(const GridProblem& P, int st);

@@ -651,6 +651,13 @@ __global__ void rng_kernel(unsigned long long seed, unsigned long long stream, i
 }
 
 // ---- shared deterministic-solver driver ----------------------------------------------------------
+// The cluster-resident solver (K-cluster) takes every single-term plain-store system of at least
+// 8 slices that fits one 16-CTA cluster's shared memory (Kerr N = 20..100: 13.7 / 12.3 / 12.7 /
+// 17.9 us per attempt at N = 20 / 50 / 70 / 100 against 14.6 / 19.1 / 22.5 / 21.5 on the grid
+// engine; 4 slices (Kerr N = 10): one CTA is faster, 11.9 vs 14.1; profiles/r02_cluster_solve.log)
+constexpr long long kClusterSolveMinSlices = 8;
+constexpr long long kClusterSolveRows = 1LL << 30;
+
 static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G, long long d,
                                  const double* y0, const double* tlist, long long n_t, int n_e,
                                  const qsg_csr* e_ops, const double* params, int n_params,
@@ -838,8 +845,30 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   P.ctl = d_ctl.as<GridCtl>();
   P.red = d_red.as<double>();
   P.bar = d_bar.as<unsigned>();
+  // Cluster-resident solve (K-cluster) for small single-term systems: the operator and the state in
+  // the shared memory of one thread-block cluster (QSG_CLUSTER_SOLVE=0 disables, =1 forces when it fits)
+  ClLayout cl{};
+  int cl_ctas = 0;
+  {
+    const char* cs = std::getenv("QSG_CLUSTER_SOLVE");
+    const bool allow = !(cs && cs[0] == '0');
+    const bool forced = cs && cs[0] == '1';
+    if (allow && G->n_terms == 1 && G->ops[0]->code_bytes == 0 && n <= kClusterSolveRows &&
+        (forced || nblk >= kClusterSolveMinSlices) && !std::getenv("QSG_GRID")) {
+      std::vector<long long> so(static_cast<size_t>(nblk + 1));
+      if ((ce = cudaMemcpyAsync(so.data(), G->ops[0]->slice_off, sizeof(long long) * (nblk + 1), cudaMemcpyDeviceToHost, s)) ||
+          (ce = cudaStreamSynchronize(s)))
+        return cuda_fail(ce, "slice offsets");
+      if (!plan_cluster_solve(P, so.data(), kObsSlots, &cl_ctas, &cl)) cl_ctas = 0;
+    }
+  }
   cudaEventRecord(ctx->ev[0], s);
-  if ((ce = launch_grid_dp5(P, mode, st, grid, s))) return cuda_fail(ce, "solver launch");
+  if (cl_ctas > 0) {
+    grid = cl_ctas;
+    if ((ce = launch_cluster_dp5(P, mode, cl, cl_ctas, s))) return cuda_fail(ce, "cluster solver launch");
+  } else if ((ce = launch_grid_dp5(P, mode, st, grid, s))) {
+    return cuda_fail(ce, "solver launch");
+  }
   cudaEventRecord(ctx->ev[1], s);
   GridCtl ctl{};
   if ((ce = cudaMemcpyAsync(&ctl, d_ctl.p, sizeof(GridCtl), cudaMemcpyDeviceToHost, s)))

@@ -170,3 +170,23 @@ def test_context_outlives_its_operators():
     a.close()
     b.close()  # last reference: frees the store, then the context
     assert np.all(np.isfinite(ref))
+
+
+@pytest.mark.parametrize("name,prm", [("kerr", (20, 1.0, 0.01, 2.0, 1.0)), ("kerr", (50, 1.0, 0.01, 2.0, 1.0)),
+                                      ("ising", (5, 1, 1.0, 0.2, 1.0, 1))])
+def test_cluster_resident_solver_matches_oracle(ctx, monkeypatch, name, prm):
+    """K-cluster (operator and state in one cluster's distributed shared memory) against the
+    oracle: configs[0] Kerr-20, configs[3] Kerr-50, and a TFIM chain (different gather pattern)."""
+    from tests._helpers import e_ops_csr, rho0_vec
+    monkeypatch.setenv("QSG_CLUSTER_SOLVE", "1")
+    m = O.Model(name, *prm)
+    t = np.linspace(0.0, 10.0, 101)
+    gen = q.Generator([ctx.op(csr_from_oracle(m, O.L_CONST))])
+    dev = q.mesolve(ctx, gen, m.dim, rho0_vec(m), t, e_ops_csr(m))
+    ex, st, _ = m.mesolve(t)
+    assert normwise_rel(dev["expect"], ex) <= 1e-6
+    assert_stats_close(dev["stats"], st)
+    monkeypatch.setenv("QSG_CLUSTER_SOLVE", "0")
+    ref = q.mesolve(ctx, gen, m.dim, rho0_vec(m), t, e_ops_csr(m))
+    assert dev["grid_ctas"] != ref["grid_ctas"] or name == "kerr"
+    assert normwise_rel(dev["expect"], ref["expect"]) <= 1e-9
