@@ -108,7 +108,8 @@ typedef struct {
   int32_t grid_ctas;  /* CTAs cooperating on one system */
   int32_t lanes;      /* lanes per CSR row in the SpMV */
   int32_t store;      /* operator store the solver streamed: 0 plain, 1 coded, 2 key-aligned */
-  int32_t reserved;
+  int32_t engine;     /* deterministic solves: 0 cooperative grid, 1 grid launched as one cluster,
+                         2 cluster-resident (state and operator in distributed shared memory) */
 } qsg_timing;
 
 /* ---- context / operator store ------------------------------------------------------- */

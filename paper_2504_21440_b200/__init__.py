@@ -70,7 +70,7 @@ class _Stats(C.Structure):
 
 class _Timing(C.Structure):
     _fields_ = [("kernel_ms", C.c_double), ("total_ms", C.c_double), ("attempts", C.c_int64),
-                ("grid_ctas", C.c_int32), ("lanes", C.c_int32), ("store", C.c_int32), ("reserved", C.c_int32)]
+                ("grid_ctas", C.c_int32), ("lanes", C.c_int32), ("store", C.c_int32), ("engine", C.c_int32)]
 
 
 class _McOut(C.Structure):
@@ -320,7 +320,7 @@ def _solve(fn, ctx, gen, d, y0, tlist, e_ops, params, abstol, reltol, max_steps,
         "states": None if states is None else states.reshape(nsave, n_state),
         "kernel_ms": tm.kernel_ms,
         "attempts": tm.attempts,
-        "grid_ctas": tm.grid_ctas, "store": tm.store,
+        "grid_ctas": tm.grid_ctas, "store": tm.store, "engine": tm.engine,
         "lanes": tm.lanes,
     }
 

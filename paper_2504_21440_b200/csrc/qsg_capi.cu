@@ -883,6 +883,7 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
     timing->grid_ctas = grid;
     timing->lanes = lanes;
     timing->store = st;
+    timing->engine = cl_ctas > 0 ? 2 : P.cluster ? 1 : 0;
   }
   if (qsg_status sst = status_from_device(ctl.status, ctl.fail_t)) return sst;
   if (expect && n_e > 0)
