@@ -120,7 +120,8 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_init():
+def dist_init(gpu=True):
+    """One process per GPU (NCCL); the CPU reference arm joins with gloo (no device needed)."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -128,8 +129,11 @@ def dist_init():
         import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gpu:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     return ws, rank, local
 
 
@@ -557,15 +561,22 @@ def mcsolve_sharded(args, ctx, q, torch, ws, rank, peak, cpu=False):
     b, e, leaves = shards[rank]
     rel = [(lo - b, hi - b) for lo, hi in leaves]  # leaf positions in this rank's completed list
     q.mcsolve(ctx, G, cops, eops, m.dim, m.psi0(), TLIST, MC_SEED, b, min(e, b + 64), per_traj=False)  # warm-up
-    comm = ProductComm(ctx, rank, ws) if ws > 1 else None
+    comm, comm_note = None, None
+    if ws > 1:
+        try:
+            comm = ProductComm(ctx, rank, ws)
+        except Exception as ex:  # keep the line: torch.distributed (NCCL) all-gather instead
+            comm_note = f"product NCCL communicator unavailable ({ex}); torch.distributed all_gather used"
     barrier(ws)
     r = q.mcsolve(ctx, G, cops, eops, m.dim, m.psi0(), TLIST, MC_SEED, b, e, per_traj=False, ranges=rel)
     t_ms = allreduce_max(r["kernel_ms"], ws)
     att_all = allreduce_sum(r["attempts"], ws)
     if ws > 1:
         nl = max(len(s[2]) for s in shards)
-        sums, counts = gather_leaf_sums(r["range_sums"], r["n_ok"], nl, ws, comm=comm)
-        comm.close()
+        sums, counts = gather_leaf_sums(r["range_sums"], r["n_ok"], nl, ws, comm=comm,
+                                        device=torch.device("cuda", ctx.device))
+        if comm is not None:
+            comm.close()
     else:
         sums, counts = [r["range_sums"]], [r["n_ok"]]
     n_ok = sum(counts)
@@ -578,7 +589,7 @@ def mcsolve_sharded(args, ctx, q, torch, ws, rank, peak, cpu=False):
            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                         "bytes_model": "47*16*n per trajectory-attempt (SURVEY.md 8d), operator L2-resident"},
            "shards": "whole pairwise-bracket subtrees per rank (dist.ensemble_shards), sums on the device",
-           "collective": "product NCCL all-gather (qsg_comm_allgather) of per-rank bracket-subtree sums"
+           "collective": (comm_note or "product NCCL all-gather (qsg_comm_allgather) of per-rank bracket-subtree sums")
                          if ws > 1 else None}
     if cpu:
         from oracle import oracle as O
@@ -594,12 +605,13 @@ def mcsolve_sharded(args, ctx, q, torch, ws, rank, peak, cpu=False):
     return res
 
 
-def oracle_tfim10(threads):
+def oracle_tfim10(threads, spins=10):
     """The oracle's TFIM-10 model with the Liouvillian prebuilt (the reference builds it inside
-    mesolve, evolve.cpp:243-252; the GPU line times the device assembly separately too)."""
+    mesolve, evolve.cpp:243-252; the GPU line times the device assembly separately too).
+    spins != 10 only through the --ref-sample-spins test hook."""
     from oracle import oracle as O
     O.set_threads(threads)
-    m = O.Model("ising", *TFIM)
+    m = O.Model("ising", spins, *TFIM[1:])
     t0 = time.perf_counter()
     m.prepare_liouvillian()
     return O, m, time.perf_counter() - t0
@@ -626,7 +638,7 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return None
     th = host_threads()
-    O, m, build = oracle_tfim10(th)
+    O, m, build = oracle_tfim10(th, args.ref_sample_spins)
     for _ in range(args.warmup):
         m.mesolve_prepared(TLIST)
     vals = []
@@ -673,9 +685,11 @@ def main():
     ap.add_argument("--sde-traj", type=int, default=2000)
     ap.add_argument("--quick", action="store_true", help="headline only (no secondary workloads)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--ref-sample-spins", type=int, default=10,
+                    help=argparse.SUPPRESS)  # test hook: a smaller chain for the CPU launch test
     args = ap.parse_args()
     maybe_relaunch(args)
-    ws, rank, local = dist_init()
+    ws, rank, local = dist_init(gpu=args.impl != "reference")
     if ws != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
