@@ -82,14 +82,28 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   if (P.n >= 4096 && n_sys * 3 < slots1) layout = 1;
   if (const char* m = std::getenv("QSG_BATCH_MODE")) {
     const std::string v(m);
-    layout = v == "grid"       ? 1
-             : v == "local"    ? 0
-             : v == "local4"   ? 2
-             : v == "local2"   ? 3
-             : v == "cluster1" ? 5
-             : v == "cluster2" ? 6
-                               : 4;
+    layout = v == "grid"        ? 1
+             : v == "local"     ? 0
+             : v == "local4"    ? 2
+             : v == "local2"    ? 3
+             : v == "cluster1"  ? 5
+             : v == "cluster2"  ? 6
+             : v == "clusterdsm" ? 7
+                                : 4;
   }
+  // layout 7 (one trajectory per cluster, its state in the cluster's shared memory): the rows per
+  // CTA are a power of two so a gather's owner CTA is a shift; up to 16 CTAs of ~200 KB each
+  int dsm_shift = 0, dsm_cs = 0;
+  {
+    int sh = 5;
+    while ((1LL << sh) * 16 < P.n) ++sh;
+    const int cs7 = static_cast<int>((P.n + (1LL << sh) - 1) >> sh);
+    if (batch_dsm_smem(sh) <= 200u * 1024u && cs7 >= 1 && cs7 <= 16) {
+      dsm_shift = sh;
+      dsm_cs = cs7;
+    }
+  }
+  if (layout == 7 && dsm_cs == 0) layout = 4;
   int cs = 16;
   // mesolve parameter sweeps (configs[4]): one point per cluster of cs CTAs, cs the smallest size
   // whose co-resident points' state fits 1.5x L2 while every CTA slot still has work (16 when
@@ -111,8 +125,13 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
     }
   }
   if (const char* c = std::getenv("QSG_CLUSTER")) cs = std::max(1, std::min(16, std::atoi(c)));
+  if (layout == 7) cs = dsm_cs;
+  if (layout == 7) {
+    cs = dsm_cs;
+    P.dsm_shift = dsm_shift;
+  }
   const bool grid_mode = layout == 1;
-  const bool cluster_mode = layout == 5 || layout == 6;
+  const bool cluster_mode = layout == 5 || layout == 6 || layout == 7;
   const int per_sm = batch_max_blocks_per_sm(layout);
   if (per_sm <= 0) return cuda_fail(cudaGetLastError(), "batch occupancy");
   const long long want = (n_sys + batch_slots(layout) - 1) / batch_slots(layout);  // batches
@@ -120,7 +139,7 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   if (grid_mode) {
     grid = std::min(per_sm * ctx->sm_count, (P.n + 31) / 32);
   } else if (cluster_mode) {
-    const int cap = batch_max_clusters(layout, cs);
+    const int cap = batch_max_clusters(layout, layout == 7 ? cs | (dsm_shift << 8) : cs);
     if (cap <= 0) return cuda_fail(cudaGetLastError(), "cluster occupancy");
     grid = static_cast<int>(std::min<long long>(cap, want)) * cs;
   } else {

@@ -55,9 +55,14 @@ struct BatchProblem {
   double* gpart;  // (32 slots x 15 values) x G partials
   double* gfin;   // 32 x 15 totals
   unsigned* bar;  // {count, generation}
+  // layout 7 (state resident in the cluster's distributed shared memory): each CTA of a cluster
+  // owns 1 << dsm_shift rows of every state array, in its shared memory
+  int dsm_shift;
 };
 
 int batch_slots(int layout);
+// layout 7: dynamic shared memory per CTA for 1 << shift rows of the 12 state arrays
+size_t batch_dsm_smem(int shift);
 // cs: CTAs per cluster (cluster layouts 5/6 only); grid must then be a multiple of cs
 cudaError_t launch_batch(const BatchProblem& P, int layout, int grid, int cs, cudaStream_t s);
 int batch_max_clusters(int layout, int cs);  // co-resident clusters of cs CTAs

@@ -52,7 +52,10 @@ enum Src { SRC_DENSE = 0, SRC_Y = 1, SRC_SC = 2 };
 //               separated by software grid barriers.
 //   GM_CLUSTER: one batch per thread-block cluster, rows partitioned over the cluster's CTAs,
 //               passes separated by hardware cluster barriers, slot reductions through DSMEM.
-enum GroupMode { GM_CTA = 0, GM_GRID = 1, GM_CLUSTER = 2 };
+//   GM_DSM:     as GM_CLUSTER, but every state array lives in the shared memory of the CTA that
+//               owns the rows (1 << dsm_shift each); gathers read the owner's shared memory
+//               (DSMEM), so no pass touches L2 for the state.
+enum GroupMode { GM_CTA = 0, GM_GRID = 1, GM_CLUSTER = 2, GM_DSM = 3 };
 
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -137,28 +140,48 @@ __device__ double rng_uniform_pos(unsigned long long* s) {
 
 // Logical buffer k of slot s lives in physical array map[s][k]: an accepted step relabels
 // (Y, YO, Y1) and (K1, K1O, K7) instead of copying them (FSAL, integrator.hpp:135-137).
-template <int BS, bool NA = true>
+template <int BS, bool NA = true, bool DSM = false>
 struct Ctx {
   const BatchProblem& P;
-  double2* w;  // batch workspace: NBUF arrays of [n][BS]
+  double2* w;  // batch workspace: NBUF arrays of [n][BS] (DSM: this CTA's rows, in shared memory)
   int n;
   const unsigned char (*map)[NBUF];  // shared memory, per slot
-  __device__ double2* buf(int k, int s) const { return w + static_cast<long long>(map[s][k]) * n * BS; }
+  int shift = 0, r_lo = 0;           // DSM: rows per CTA = 1 << shift, first row of this CTA
+  __device__ double2* buf(int k, int s) const {
+    if constexpr (DSM) return w + (static_cast<long long>(map[s][k]) << shift) * BS;
+    else return w + static_cast<long long>(map[s][k]) * n * BS;
+  }
+  __device__ long long at(int r, int s) const {
+    if constexpr (DSM) return static_cast<long long>(r - r_lo) * BS + s;
+    else return static_cast<long long>(r) * BS + s;
+  }
   // ld: operands streamed once per pass (NA: L1::no_allocate keeps L1 for the gathers; measured
   // +1.8% on TFIM-14 mcsolve, -2.4% on the cluster-layout sweep, so cluster layouts keep L1
-  // allocation); ldx: gathers and dense-output reads (L1-allocating)
+  // allocation); ldx: gathers and dense-output reads (L1-allocating; DSM: from the owner CTA)
   __device__ double2 ld(int k, int r, int s) const {
-    const double2* p = buf(k, s) + static_cast<long long>(r) * BS + s;
-    if constexpr (NA) return ld_na_c2(p);
+    const double2* p = buf(k, s) + at(r, s);
+    if constexpr (NA && !DSM) return ld_na_c2(p);
     else return *p;
   }
-  __device__ double2 ldx(int k, int r, int s) const { return buf(k, s)[static_cast<long long>(r) * BS + s]; }
-  __device__ void st(int k, int r, int s, double2 v) const { buf(k, s)[static_cast<long long>(r) * BS + s] = v; }
+  __device__ double2 ldx(int k, int c, int s) const {
+    if constexpr (DSM) {
+      const unsigned owner = static_cast<unsigned>(c) >> shift;
+      const double2* p = buf(k, s) + (static_cast<long long>(c & ((1 << shift) - 1)) * BS + s);
+      unsigned la = static_cast<unsigned>(__cvta_generic_to_shared(p)), ra;
+      double2 v;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(owner));
+      asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(ra) : "memory");
+      return v;
+    } else {
+      return buf(k, s)[static_cast<long long>(c) * BS + s];
+    }
+  }
+  __device__ void st(int k, int r, int s, double2 v) const { buf(k, s)[at(r, s)] = v; }
 };
 
 // dense output of slot s at index c (integrator.hpp:127-131,150-154) from the committed step
-template <int BS, bool NA>
-__device__ __forceinline__ double2 dense_at(const Ctx<BS, NA>& C, int c, int s, double theta, double h, int src) {
+template <int BS, bool NA, bool DSM>
+__device__ __forceinline__ double2 dense_at(const Ctx<BS, NA, DSM>& C, int c, int s, double theta, double h, int src) {
   if (src == SRC_Y) return C.ldx(Y, c, s);
   if (src == SRC_SC) return C.ldx(SC, c, s);
   using namespace dp;
@@ -327,17 +350,23 @@ __device__ void slot_reduce(const BatchProblem& P, double (&acc)[NA], double* sr
     out[ss * NA + a] = v;
   }
   __syncthreads();
-  if constexpr (GM == GM_CLUSTER) {
+  if constexpr (GM == GM_CLUSTER || GM == GM_DSM) {
     // every CTA publishes its totals in its own shared memory (double-buffered by the caller, so
     // the next reduction cannot overwrite a buffer another CTA is still reading), then sums the
-    // cluster's totals in rank order: identical results in every CTA of the cluster.
+    // cluster's totals in rank order: identical results in every CTA of the cluster. The (<= 16)
+    // remote loads are all issued before the in-order sum, so their latencies overlap.
     const int cnt = BS * NA;
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) pub[i] = out[i];
     cluster_sync_all();
     const unsigned cs = cluster_size();
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      double t[16];
+#pragma unroll
+      for (unsigned r = 0; r < 16; ++r) t[r] = r < cs ? dsmem_ld(pub + i, r) : 0.0;
       double v = 0.0;
-      for (unsigned r = 0; r < cs; ++r) v += dsmem_ld(pub + i, r);
+#pragma unroll
+      for (unsigned r = 0; r < 16; ++r)
+        if (r < cs) v += t[r];
       out[i] = v;
     }
     __syncthreads();
@@ -398,7 +427,8 @@ __device__ bool has_more(const Slot& s, const BatchProblem& P) {
 template <int BS, int GM>
 __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const __grid_constant__ BatchProblem P) {
   constexpr bool GRID = GM == GM_GRID;
-  constexpr bool CLU = GM == GM_CLUSTER;
+  constexpr bool DSM = GM == GM_DSM;
+  constexpr bool CLU = GM == GM_CLUSTER || DSM;
   constexpr bool PART = GM != GM_CTA;  // rows partitioned over the CTAs of a group
   constexpr int B = BS;
   constexpr int RPW = 32 / BS;
@@ -417,12 +447,16 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
   const int g_rank = GRID ? static_cast<int>(blockIdx.x) : CLU ? static_cast<int>(cluster_rank()) : 0;
   const int g_size = GRID ? static_cast<int>(gridDim.x) : CLU ? static_cast<int>(cluster_size()) : 1;
   const long long batch_id = GRID ? 0LL : CLU ? static_cast<long long>(blockIdx.x) / g_size : blockIdx.x;
-  const Ctx<BS, !CLU> C{P, P.work + batch_id * P.work_stride, n, s_map};
+  // DSM: the state arrays follow the reduction scratch in dynamic shared memory (16-B aligned)
+  double2* const dsm_w = reinterpret_cast<double2*>(
+      reinterpret_cast<unsigned char*>(sred) + ((static_cast<size_t>(W) * BS * 15 * sizeof(double) + 15) & ~size_t(15)));
+  const int rows_dsm = 1 << P.dsm_shift;
   const double atol = P.atol, rtol = P.rtol, eps_t = P.eps_t, tf = P.tf, t0 = P.t0;
   const bool out_cta = g_rank == 0;  // the CTA of a group that writes per-system outputs
-  const int rpc = PART ? (n + g_size - 1) / g_size : n;
+  const int rpc = DSM ? rows_dsm : PART ? (n + g_size - 1) / g_size : n;
   const int r_lo = PART ? min(n, g_rank * rpc) : 0;
   const int r_hi = PART ? min(n, r_lo + rpc) : n;
+  const Ctx<BS, !CLU, DSM> C{P, DSM ? dsm_w : P.work + batch_id * P.work_stride, n, s_map, P.dsm_shift, r_lo};
   int pub_par = 0;
   auto rows = [&](auto&& f) {
     for (int r = r_lo + warp * RPW + rs; r < r_hi; r += W * RPW) f(r);
@@ -433,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
     const int step = W * RPW;
     for (int r = r_lo + warp * RPW + rs; r < r_hi; r += step) {
       const int rn = r + step;
-      if (rn < r_hi)
+      if (!DSM && rn < r_hi)
         for (int k = 0; k < NBUF; ++k)
           if ((mask >> k) & 1u) prefetch_row(C.buf(k, sl) + static_cast<long long>(rn) * BS + sl);
       f(r);
@@ -1063,6 +1097,28 @@ int cluster_capacity(int cs) {
   return nc;
 }
 
+// GM_DSM: the reduction scratch plus the 12 state arrays of this CTA's 1 << shift rows
+size_t dsm_smem_bytes(int shift) {
+  return ((static_cast<size_t>(W) * 15 * sizeof(double) + 15) & ~size_t(15)) +
+         static_cast<size_t>(NBUF) * (size_t(1) << shift) * sizeof(double2);
+}
+
+cudaLaunchConfig_t dsm_cfg(int grid, int cs, size_t smem, cudaLaunchAttribute* at) {
+  cudaFuncSetAttribute(batch_kernel<1, GM_DSM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(batch_kernel<1, GM_DSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
 }  // namespace
 }  // namespace qsg
 
@@ -1072,16 +1128,36 @@ namespace {
 // translation unit instantiates exactly one kernel.
 template <int BS, int GM>
 int layout_occ() {
-  return occupancy_of<BS, GM>();
+  if constexpr (GM == GM_DSM) return 1;
+  else return occupancy_of<BS, GM>();
 }
+// cs CTAs per cluster; GM_DSM: cs = clusters' CTA count with `shift` rows each (shift in cs >> 8)
 template <int BS, int GM>
 int layout_clusters(int cs) {
-  if constexpr (GM == GM_CLUSTER) return cluster_capacity<BS>(cs);
-  else return 0;
+  if constexpr (GM == GM_CLUSTER) {
+    return cluster_capacity<BS>(cs);
+  } else if constexpr (GM == GM_DSM) {
+    const int c = cs & 0xff, shift = cs >> 8;
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t cfg = dsm_cfg(c * 64, c, dsm_smem_bytes(shift), at);
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, batch_kernel<1, GM_DSM>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return nc;
+  } else {
+    return 0;
+  }
 }
 template <int BS, int GM>
 cudaError_t layout_launch(const BatchProblem& P, int grid, int cs, cudaStream_t s) {
-  if constexpr (GM == GM_CLUSTER) {
+  if constexpr (GM == GM_DSM) {
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t cfg = dsm_cfg(grid, cs, dsm_smem_bytes(P.dsm_shift), at);
+    cfg.stream = s;
+    return cudaLaunchKernelEx(&cfg, batch_kernel<1, GM_DSM>, P);
+  } else if constexpr (GM == GM_CLUSTER) {
     return launch_cluster<BS>(P, grid, cs, s);
   } else if constexpr (GM == GM_GRID) {
     void* args[] = {const_cast<BatchProblem*>(&P)};

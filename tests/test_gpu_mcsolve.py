@@ -275,3 +275,14 @@ def test_device_bracket_sums_large_ensemble(ctx):
     assert np.array_equal(r["block_sum"].view(np.float64), _pairwise(per, 0, 5000).view(np.float64))
     for (lo, hi), s in zip([(0, 2500), (2500, 5000), (17, 4099)], r["range_sums"]):
         assert np.array_equal(s.view(np.float64), _pairwise(per, lo, hi).view(np.float64))
+
+
+def test_cluster_dsm_layout_matches_oracle(ctx, monkeypatch):
+    """Batch layout 7 (one trajectory per cluster, state in distributed shared memory): same
+    trajectories as the oracle (TFIM-7 chain, seed 2025)."""
+    monkeypatch.setenv("QSG_BATCH_MODE", "clusterdsm")
+    m = O.Model("ising", 7, 1, 1.0, 0.2, 1.0, 1)
+    t = np.linspace(0, 10, 100)
+    dev = _mc(ctx, m, t, 2025, 0, 24)
+    ref = m.mcsolve(t, 2025, 24)
+    _compare_trajectories(dev, ref)
