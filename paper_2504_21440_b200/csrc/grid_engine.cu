@@ -44,6 +44,9 @@ enum { Y = 0, YO = 1, K1 = 2, K2 = 3, K3 = 4, K4 = 5, K5 = 6, K6 = 7, K7 = 8, SA
 // Integrator state of the solve — identical in every CTA, written by thread 0 only.
 struct Ctl {
   double2* p[11];  // logical -> physical buffer (FSAL / y rotation, integrator.hpp:133-138)
+  const double* ev_t;  // event times / grid index / save index (P.ev_*, or a shared-memory copy)
+  const int* ev_grid;
+  const int* ev_save;
   double t, t_old, h, h_last, facold, hh, h0, d1;
   double fail_t;
   long long steps, rejected, rhs_evals, attempts_total;
@@ -179,7 +182,7 @@ __device__ __forceinline__ void sync_all(const GridProblem& P, int G) {
 }
 
 __device__ __forceinline__ void push_pending(const GridProblem& P, Ctl& c, double theta) {
-  c.pend[c.np] = Pending{theta, P.ev_grid[c.next], P.ev_save[c.next]};
+  c.pend[c.np] = Pending{theta, c.ev_grid[c.next], c.ev_save[c.next]};
   ++c.np;
   ++c.next;
 }
@@ -618,9 +621,9 @@ __device__ void finish_attempt(const GridProblem& P, Ctl& c, double err_sq, int 
     ++c.steps;
     c.h = c.clamped ? fmax(c.h, h_new) : h_new;
     c.attempts = 0;
-    while (c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t && c.np < kcap)
-      push_pending(P, c, (fmin(P.ev_t[c.next], c.t) - c.t_old) / c.h_last);
-    const bool more = c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t;
+    while (c.next < P.n_ev && c.ev_t[c.next] <= c.t + P.eps_t && c.np < kcap)
+      push_pending(P, c, (fmin(c.ev_t[c.next], c.t) - c.t_old) / c.h_last);
+    const bool more = c.next < P.n_ev && c.ev_t[c.next] <= c.t + P.eps_t;
     const bool last = c.t >= P.tf - P.eps_t;
     c.flush = more || (last && c.np > 0);
     c.done = last || c.next >= P.n_ev;
@@ -662,6 +665,9 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 11; ++i) c.p[i] = P.buf[i];
+    c.ev_t = P.ev_t;
+    c.ev_grid = P.ev_grid;
+    c.ev_save = P.ev_save;
     c.t = c.t_old = P.t0;
     c.h = c.h_last = 0.0;
     c.facold = 1e-4;
@@ -670,7 +676,7 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     c.attempts = c.next = c.np = c.obs_par = c.flush = c.done = 0;
     c.fail_t = 0.0;
     // events at t0 observe y0 directly (evolve.cpp:134-137)
-    while (c.next < P.n_ev && P.ev_t[c.next] <= P.t0 + P.eps_t && c.np < kcap)
+    while (c.next < P.n_ev && c.ev_t[c.next] <= P.t0 + P.eps_t && c.np < kcap)
       push_pending(P, c, __longlong_as_double(0x7ff8000000000000ll));
   }
   __syncthreads();
@@ -823,9 +829,9 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     while (c.flush) {  // pending list full, or the solve ends with events pending
       flush_obs();
       if (threadIdx.x == 0) {
-        while (c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t && c.np < kcap)
-          push_pending(P, c, (fmin(P.ev_t[c.next], c.t) - c.t_old) / c.h_last);
-        const bool more = c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t;
+        while (c.next < P.n_ev && c.ev_t[c.next] <= c.t + P.eps_t && c.np < kcap)
+          push_pending(P, c, (fmin(c.ev_t[c.next], c.t) - c.t_old) / c.h_last);
+        const bool more = c.next < P.n_ev && c.ev_t[c.next] <= c.t + P.eps_t;
         c.flush = more || (c.t >= P.tf - P.eps_t && c.np > 0);
       }
       __syncthreads();
@@ -875,6 +881,7 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
 // (Ctl, begin_attempt, finish_attempt), replicated identically in every CTA; reductions are CTA
 // partials read by every CTA from every CTA's shared memory in rank order (deterministic).
 constexpr int kClThreads = 512;
+constexpr int kEvSmem = 1024;  // events staged in shared memory when the solve has at most this many
 
 __device__ __forceinline__ unsigned cl_rank() {
   unsigned r;
@@ -1049,8 +1056,23 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
       val[(soff[sl] + j) * 32 + lane] = __ldg(A.val + gi);
     }
   }
+  // events in shared memory (L1 is invalidated by every cluster barrier, so the controller would
+  // otherwise fetch them from L2 on each accepted step)
+  __shared__ double s_evt[kEvSmem];
+  __shared__ int s_evg[kEvSmem], s_evs[kEvSmem];
+  const bool ev_sm = P.n_ev <= kEvSmem;
+  if (ev_sm)
+    for (int i = threadIdx.x; i < P.n_ev; i += kClThreads) {
+      s_evt[i] = P.ev_t[i];
+      s_evg[i] = P.ev_grid[i];
+      s_evs[i] = P.ev_save[i];
+    }
+  __syncthreads();
   if (threadIdx.x == 0) {
     for (int i = 0; i < 11; ++i) c.p[i] = vec + static_cast<long long>(i) * R;
+    c.ev_t = ev_sm ? s_evt : P.ev_t;
+    c.ev_grid = ev_sm ? s_evg : P.ev_grid;
+    c.ev_save = ev_sm ? s_evs : P.ev_save;
     c.t = c.t_old = P.t0;
     c.h = c.h_last = 0.0;
     c.facold = 1e-4;
@@ -1058,7 +1080,7 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
     c.status = kRunning;
     c.attempts = c.next = c.np = c.obs_par = c.flush = c.done = 0;
     c.fail_t = 0.0;
-    while (c.next < P.n_ev && P.ev_t[c.next] <= P.t0 + P.eps_t && c.np < kcap)
+    while (c.next < P.n_ev && c.ev_t[c.next] <= P.t0 + P.eps_t && c.np < kcap)
       push_pending(P, c, __longlong_as_double(0x7ff8000000000000ll));
   }
   __syncthreads();
@@ -1336,9 +1358,9 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
     while (c.flush) {
       flush();
       if (threadIdx.x == 0) {
-        while (c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t && c.np < kcap)
-          push_pending(P, c, (fmin(P.ev_t[c.next], c.t) - c.t_old) / c.h_last);
-        const bool more = c.next < P.n_ev && P.ev_t[c.next] <= c.t + P.eps_t;
+        while (c.next < P.n_ev && c.ev_t[c.next] <= c.t + P.eps_t && c.np < kcap)
+          push_pending(P, c, (fmin(c.ev_t[c.next], c.t) - c.t_old) / c.h_last);
+        const bool more = c.next < P.n_ev && c.ev_t[c.next] <= c.t + P.eps_t;
         c.flush = more || (c.t >= P.tf - P.eps_t && c.np > 0);
       }
       __syncthreads();
@@ -1512,7 +1534,8 @@ bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, i
     L.red = o;
     o = al(o + 8u * (4 + 2 * n_obs_slots));  // control sums + two observation banks
     L.bytes = o;
-    const unsigned static_smem = sizeof(double) * (kClThreads / 32) + sizeof(Ctl);
+    const unsigned static_smem = sizeof(double) * (kClThreads / 32) + sizeof(Ctl) + kEvSmem * 16u +
+                                 (kClThreads / 32) * 16 * 8 + 64;
     // the smallest cluster whose per-CTA share fits (more CTAs only add DSMEM hops and barrier
     // arrivals); 16 slices per CTA at most so every warp owns at most one slice per pass
     if (L.bytes + static_smem <= 200u * 1024u && S <= 64 && R < (1 << 24)) {
