@@ -252,11 +252,14 @@ def run_ours(args, ws, rank, local):
         op_w.close()
     barrier(ws)
     t0 = time.perf_counter()
+    e2e_each = []
     for _ in range(e2e_steps):
+        ts = time.perf_counter()
         op2 = ctx.liouvillian(Hh, cops_h)
         r2 = q.mesolve(ctx, q.Generator([op2]), d, rho0_h, TLIST, eops)
         _ = r2["expect"].sum()
         op2.close()
+        e2e_each.append(time.perf_counter() - ts)
     e2e_s = allreduce_max((time.perf_counter() - t0) / e2e_steps, ws)
     h2d = csr_bytes(H) + sum(csr_bytes(c) for c in cops) + rho0.nbytes + sum(csr_bytes(e) for e in eops)
     d2h = r2["expect"].nbytes
@@ -348,6 +351,7 @@ def run_ours(args, ws, rank, local):
                      "store_streamed": {0: "plain", 1: "coded", 2: "key-aligned"}[int(r["store"])],
                      "store_bytes_per_spmv": stage_bytes},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "per_step_s": e2e_each,
                 "path": "qsg_liouvillian_create(pinned host H, c_ops) + qsg_mesolve(host rho0 -> host expect)"},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
