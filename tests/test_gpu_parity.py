@@ -78,7 +78,10 @@ def test_mesolve_damped_cavity_analytic(ctx):
     assert_stats_close(res["stats"], st)
 
 
-def test_mesolve_ising_states_and_saveat(ctx):
+@pytest.mark.parametrize("cluster_solve", ["0", "1"])
+def test_mesolve_ising_states_and_saveat(ctx, monkeypatch, cluster_solve):
+    """State saves and saveat events on the grid engine and on K-cluster."""
+    monkeypatch.setenv("QSG_CLUSTER_SOLVE", cluster_solve)
     m = O.Model("ising", 3, 2, 1.0, 0.2, 1.0, 1)
     t = np.linspace(0.0, 4.0, 21)
     sv = np.array([0.0, 0.33, 1.0, 2.5, 4.0])
@@ -190,3 +193,17 @@ def test_cluster_resident_solver_matches_oracle(ctx, monkeypatch, name, prm):
     ref = q.mesolve(ctx, gen, m.dim, rho0_vec(m), t, e_ops_csr(m))
     assert dev["engine"] == 2 and ref["engine"] != 2
     assert normwise_rel(dev["expect"], ref["expect"]) <= 1e-9
+
+
+def test_cluster_resident_sesolve_matches_oracle(ctx, monkeypatch):
+    """K-cluster in sesolve mode (<psi|E psi> observations gathered across the cluster): closed
+    TFIM chain of 9 spins (512 amplitudes, 16 slices), against the oracle's sesolve."""
+    monkeypatch.setenv("QSG_CLUSTER_SOLVE", "1")
+    m = O.Model("ising", 9, 1, 1.0, 0.2, 0.0, 1)
+    t = np.linspace(0.0, 5.0, 51)
+    gen = q.Generator([ctx.op(csr_from_oracle(m, O.SE_GEN))])
+    dev = q.sesolve(ctx, gen, m.dim, m.psi0(), t, e_ops_csr(m))
+    assert dev["engine"] == 2
+    ex, st, _ = m.sesolve(t)
+    assert normwise_rel(dev["expect"], ex) <= 1e-6
+    assert_stats_close(dev["stats"], st)
