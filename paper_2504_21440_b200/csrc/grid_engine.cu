@@ -955,16 +955,17 @@ __device__ __forceinline__ double2 cl_row(const int* rowlen, const int* soff, co
   const unsigned xa = smem_u32(p[xb]);
   const unsigned ya = smem_u32(p[Y]), ka = smem_u32(p[K1]);
   double2 acc = make_double2(0.0, 0.0);
-  for (int j = 0; j < len; j += 4) {
-    unsigned tg[4];
-    double2 v[4], x[4];
+  constexpr int U = 8;  // one round of DSMEM gathers for rows of up to 8 entries (Kerr: 6)
+  for (int j = 0; j < len; j += U) {
+    unsigned tg[U];
+    double2 v[U], x[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       tg[u] = j + u < len ? tgt[base + 32 * (j + u)] : 0u;
       v[u] = j + u < len ? val[base + 32 * (j + u)] : make_double2(0.0, 0.0);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       if (j + u < len) {
         const unsigned own = tg[u] >> 24, off = (tg[u] & 0xffffffu) * 16u;
         if constexpr (S2) {
@@ -978,7 +979,7 @@ __device__ __forceinline__ double2 cl_row(const int* rowlen, const int* soff, co
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
       if (j + u < len) cfma(v[u], x[u], acc);
   }
   return acc;
@@ -1538,7 +1539,7 @@ bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, i
                                  (kClThreads / 32) * 16 * 8 + 64;
     // the smallest cluster whose per-CTA share fits (more CTAs only add DSMEM hops and barrier
     // arrivals); 16 slices per CTA at most so every warp owns at most one slice per pass
-    if (L.bytes + static_smem <= 200u * 1024u && S <= 64 && R < (1 << 24)) {
+    if (L.bytes + static_smem <= 226u * 1024u && S <= 64 && R < (1 << 24)) {  // 227 KB per CTA at most
       *C_out = C;
       *plan = L;
       return true;
