@@ -1088,6 +1088,28 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
   for (int i = threadIdx.x; i < r1 - r0; i += kClThreads) c.p[Y][i] = P.buf[0][r0 + i];  // y0 (host-staged)
   cl_sync();
 
+  // mesolve e_op entries in shared memory when the plan made room (L.n_eo > 0)
+  const int* eo_off = P.eo_off;
+  const int* eo_i = P.eo_i;
+  const int* eo_j = P.eo_j;
+  const double2* eo_v = P.eo_v;
+  if (MODE == 0 && L.n_eo > 0) {
+    int* so = reinterpret_cast<int*>(s_dyn + L.eo);
+    double2* sv = reinterpret_cast<double2*>(s_dyn + L.eo + ((4u * (P.n_e + 1) + 15u) & ~15u));
+    int* si = reinterpret_cast<int*>(sv + L.n_eo);
+    int* sj = si + L.n_eo;
+    for (int i = threadIdx.x; i <= P.n_e; i += kClThreads) so[i] = P.eo_off[i];
+    for (int i = threadIdx.x; i < L.n_eo; i += kClThreads) {
+      sv[i] = P.eo_v[i];
+      si[i] = P.eo_i[i];
+      sj[i] = P.eo_j[i];
+    }
+    eo_off = so;
+    eo_i = si;
+    eo_j = sj;
+    eo_v = sv;
+    __syncthreads();
+  }
   // ---- observation pass: pending events -> expectation partials in red[4 + 2*(q*n_e+e)] and saves
   // bank of observation slots in red[] (double-buffered by c.obs_par, like the grid engine's):
   // a bank is rewritten two observation events later, after at least one more cluster barrier
@@ -1112,10 +1134,10 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
         const double th = c.pend[q].theta;
         if (c.pend[q].grid_idx < 0) continue;
         if (MODE == 0) {
-          for (int k = P.eo_off[e] + gt; k < P.eo_off[e + 1]; k += gs) {
-            const int i = P.eo_i[k], j = P.eo_j[k];
+          for (int k = eo_off[e] + gt; k < eo_off[e + 1]; k += gs) {
+            const int i = eo_i[k], j = eo_j[k];
             const double2 rji = cl_dense(p, i * P.d + j, th, hl, R), rij = cl_dense(p, j * P.d + i, th, hl, R);
-            acc[v] = cadd(acc[v], cmul(P.eo_v[k], cscale(0.5, cadd(rji, cconj(rij)))));
+            acc[v] = cadd(acc[v], cmul(eo_v[k], cscale(0.5, cadd(rji, cconj(rij)))));
           }
         } else {
           const int* rp = P.se_rowptr + static_cast<long long>(e) * (P.n + 1);
@@ -1500,7 +1522,7 @@ int grid_max_cluster(int mode, int st, size_t dyn_smem) {
 // Plans the cluster-resident layout for a single-term plain-store generator: C CTAs of R rows
 // each (R a multiple of 32), all state and operator slices in shared memory. Returns false when
 // the system does not fit one 16-CTA cluster.
-bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, int n_obs_slots, int* C_out,
+bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, int n_obs_slots, int n_eo, int* C_out,
                         ClLayout* plan) {
   if (P.gen.n_terms != 1 || P.gen.A[0].code_bytes != 0) return false;
   const int n = P.n;
@@ -1537,6 +1559,15 @@ bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, i
     L.bytes = o;
     const unsigned static_smem = sizeof(double) * (kClThreads / 32) + sizeof(Ctl) + kEvSmem * 16u +
                                  (kClThreads / 32) * 16 * 8 + 64;
+    // mesolve e_op entries {value, row, column} in shared memory when they still fit: the
+    // observation pass then reads no L2 (each cluster barrier invalidates L1)
+    L.eo = o;
+    L.n_eo = 0;
+    const unsigned eo_bytes = al(4u * (P.n_e + 1)) + al(24u * static_cast<unsigned>(n_eo));
+    if (n_eo > 0 && L.bytes + eo_bytes + static_smem <= 226u * 1024u) {
+      L.n_eo = n_eo;
+      L.bytes = o + eo_bytes;
+    }
     // the smallest cluster whose per-CTA share fits (more CTAs only add DSMEM hops and barrier
     // arrivals); 16 slices per CTA at most so every warp owns at most one slice per pass
     if (L.bytes + static_smem <= 226u * 1024u && S <= 64 && R < (1 << 24)) {  // 227 KB per CTA at most

@@ -58,10 +58,12 @@ struct ClLayout {
   int R;  // rows per CTA (multiple of 32)
   int S;  // slices per CTA = R / 32
   int E;  // entry capacity (32 * the widest CTA's summed slice widths)
-  unsigned vec, rowlen, soff, tgt, val, red, bytes;
+  int n_eo;  // mesolve e_op entries staged in shared memory (0: read from global)
+  unsigned vec, rowlen, soff, tgt, val, red, eo, bytes;
 };
-// true (and the cluster size / layout) when a single-term plain-store generator fits one cluster
-bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, int n_obs_slots, int* C_out,
+// true (and the cluster size / layout) when a single-term plain-store generator fits one cluster;
+// n_eo: mesolve e_op entries (staged in shared memory when they fit too)
+bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, int n_obs_slots, int n_eo, int* C_out,
                         ClLayout* plan);
 cudaError_t launch_cluster_dp5(const GridProblem& P, int mode, const ClLayout& L, int C, cudaStream_t s);
 

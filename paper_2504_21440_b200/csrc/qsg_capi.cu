@@ -859,7 +859,8 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
       if ((ce = cudaMemcpyAsync(so.data(), G->ops[0]->slice_off, sizeof(long long) * (nblk + 1), cudaMemcpyDeviceToHost, s)) ||
           (ce = cudaStreamSynchronize(s)))
         return cuda_fail(ce, "slice offsets");
-      if (!plan_cluster_solve(P, so.data(), kObsSlots, &cl_ctas, &cl)) cl_ctas = 0;
+      if (!plan_cluster_solve(P, so.data(), kObsSlots, mode == 0 ? static_cast<int>(eo_i.size()) : 0, &cl_ctas, &cl))
+        cl_ctas = 0;
     }
   }
   cudaEventRecord(ctx->ev[0], s);
