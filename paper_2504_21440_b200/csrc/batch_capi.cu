@@ -239,6 +239,15 @@ qsg_status common_setup(qsg_ctx* ctx, const qsg_generator* G, long long n, const
   }
   P.n = static_cast<int>(n);
   P.gen = make_devgen(G, batch_codes());
+  // time-independent generator (constant or params[i] coefficients): stage 2 can use k1 = G y
+  // (batch_kernel.cuh P1); QSG_K1G=0 keeps the two-vector gather
+  {
+    bool aut = true;
+    for (int k = 1; k < G->n_terms; ++k)
+      aut = aut && G->coeffs && (G->coeffs[k].kind == QSG_COEFF_CONST || G->coeffs[k].kind == QSG_COEFF_PARAM);
+    const char* kg = std::getenv("QSG_K1G");
+    P.autonomous = aut && !(kg && kg[0] == '0');
+  }
   // generator terms that carry a key-aligned store are read through it (ka_row_slot) unless
   // QSG_BATCH_KA=0
   if (const char* e = std::getenv("QSG_BATCH_KA"))

@@ -602,11 +602,19 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         const double hh = S[sl].hh, t = S[sl].t;
         using namespace dp;
         rows_pf((1u << Y) | (1u << K1), [&](int r) {
-          const double2 k = gen_row_slot<true>(P.gen, prm, r, t + c2 * hh, [&](int c) {
-            const double2 a = C.ldx(Y, c, sl), q = C.ldx(K1, c, sl);
-            return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
-          });
+          double2 k;
+          if (P.autonomous) {
+            // k1 = G y exactly (start / restart, FSAL, unchanged after a rejection), so
+            // k2 = G(y + h a21 k1) = k1 + (h a21) G k1: one gathered vector instead of two
+            k = gen_row_slot<true>(P.gen, prm, r, t + c2 * hh, [&](int c) { return C.ldx(K1, c, sl); });
+          } else {
+            k = gen_row_slot<true>(P.gen, prm, r, t + c2 * hh, [&](int c) {
+              const double2 a = C.ldx(Y, c, sl), q = C.ldx(K1, c, sl);
+              return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
+            });
+          }
           const double2 yy = C.ld(Y, r, sl), q1 = C.ld(K1, r, sl);
+          if (P.autonomous) k = make_double2(q1.x + (hh * a21) * k.x, q1.y + (hh * a21) * k.y);
           C.st(K2, r, sl, k);
           C.st(SA, r, sl, make_double2(yy.x + hh * (a31 * q1.x + a32 * k.x), yy.y + hh * (a31 * q1.y + a32 * k.y)));
         });

@@ -310,10 +310,13 @@ __device__ __forceinline__ double2 ka_row(const uint4* __restrict__ blk4, const 
   return acc;
 }
 
-// X2 (stage 2 only): the stage input y + h a21 k1 was materialised in SB by x2_pass, so the SpMV
-// gathers one vector instead of two.
+// X2 (stage 2 only): 0 = the SpMV gathers y + h a21 k1 on the fly (two vectors); 1 = that input was
+// materialised in SB by x2_pass (one extra streaming pass and barrier); 2 = autonomous single-term
+// generator: since k1 = G y exactly (start, FSAL k1 <- k7 = G ysti7, unchanged after a rejection),
+// k2 = G(y + h a21 k1) = k1 + (h a21) G k1, so the SpMV gathers k1 alone and the epilogue adds k1 —
+// no x2 pass, no extra barrier, one gathered vector.
 // ST: 0 generic rows, 1 coded store (software-pipelined), 2 key-aligned store through the ring.
-template <int S, int ST, bool X2 = false>
+template <int S, int ST, int X2 = 0>
 __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c, int s0, int s1,
                                              const double2* sval = nullptr, const int* soff = nullptr,
                                              KaRing* ring = nullptr) {
@@ -333,7 +336,7 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
   };
   const double2* __restrict__ y = gptr(c.p[Y]);
   const double2* __restrict__ k1 = gptr(c.p[K1]);
-  const double2* __restrict__ x = S == 2 ? (X2 ? gptr(c.p[SB]) : nullptr)
+  const double2* __restrict__ x = S == 2 ? (X2 == 1 ? gptr(c.p[SB]) : X2 == 2 ? gptr(c.p[K1]) : nullptr)
                                          : gptr((S == 3 || S == 5 || S == 7) ? c.p[SA] : c.p[SB]);
   const double2* __restrict__ pk2 = gptr(c.p[K2]);
   const double2* __restrict__ pk3 = gptr(c.p[K3]);
@@ -361,7 +364,7 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
     o.y1 = (S == 7 && ok) ? ldo(x + row) : z;
   };
   auto xin = [&](int col) {
-    if constexpr (S == 2 && !X2) {
+    if constexpr (S == 2 && X2 == 0) {
       const double2 a = y[col], q = k1[col];
       return make_double2(a.x + hh * (a21 * q.x), a.y + hh * (a21 * q.y));
     } else {
@@ -370,6 +373,10 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
   };
   auto epilogue = [&](int row, double2 k, const Ops& o) {
     const double2 yy = o.yy, q1 = o.q1, q2 = o.q2, q3 = o.q3, q4 = o.q4, q5 = o.q5, q6 = o.q6, y1 = o.y1;
+    if (S == 2 && X2 == 2) {  // k2 = k1 + (h a21) G k1
+      const double ca = hh * a21;
+      k = make_double2(q1.x + ca * k.x, q1.y + ca * k.y);
+    }
     if (S == 2) {
       kout[row] = k;
       xout[row] = make_double2(yy.x + hh * (a31 * q1.x + a32 * k.x), yy.y + hh * (a31 * q1.y + a32 * k.y));
@@ -790,10 +797,12 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     __syncthreads();
     if (c.done || c.status != kRunning) break;
     // stage 2 (+ observations of the previous accepted step)
-    if (PF && P.x2) {
+    if (P.k1g) {
+      stage_pass<2, ST, 2>(P, c, s0, s1, sval, soff, &ring);
+    } else if (PF && P.x2) {
       x2_pass(P, c, s0, s1);
       sync_all(P, G);
-      stage_pass<2, ST, true>(P, c, s0, s1, sval, soff, &ring);
+      stage_pass<2, ST, 1>(P, c, s0, s1, sval, soff, &ring);
     } else {
       stage_pass<2, ST == 2 ? 1 : ST>(P, c, s0, s1, sval, soff, &ring);
     }
@@ -1318,10 +1327,14 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
       double2* const* p = c.p;
       for (int sl = warp; sl < nsl; sl += W) {
         const int lr = sl * 32 + lane;
-        const double2 k = S == 2 ? cl_row<true>(rowlen, soff, tgt, val, sl, lane, p, Y, hh)
-                                 : cl_row<false>(rowlen, soff, tgt, val, sl, lane, p, xb, hh);
+        // stage 2 of an autonomous single-term generator: k2 = k1 + (h a21) G k1 (k1 = G y exactly),
+        // one gathered vector instead of y and k1 (the grid engine's X2 = 2 form)
+        double2 k = S == 2 ? (P.k1g ? cl_row<false>(rowlen, soff, tgt, val, sl, lane, p, K1, hh)
+                                    : cl_row<true>(rowlen, soff, tgt, val, sl, lane, p, Y, hh))
+                           : cl_row<false>(rowlen, soff, tgt, val, sl, lane, p, xb, hh);
         if (r0 + lr >= r1) continue;
         const double2 yy = p[Y][lr], q1 = p[K1][lr];
+        if (S == 2 && P.k1g) k = make_double2(q1.x + (hh * a21) * k.x, q1.y + (hh * a21) * k.y);
         p[ko][lr] = k;
         if (S == 2) {
           p[xo][lr] = make_double2(yy.x + hh * (a31 * q1.x + a32 * k.x), yy.y + hh * (a31 * q1.y + a32 * k.y));

@@ -23,6 +23,7 @@ struct GridProblem {
   int cluster;    // 1: the whole grid is one thread-block cluster (hardware cluster barriers)
   int smem_dict;  // > 0: the single-term coded generator's dictionary (entries) staged in shared memory
   int x2;         // materialise the stage-2 input (one extra pass + barrier, half the stage-2 gathers)
+  int k1g;        // autonomous single-term generator: stage 2 as k1 + (h a21) G k1 (no x2 pass)
   int n;     // vector length (d*d for mesolve, d for sesolve)
   int d;     // Hilbert dimension
   DevGen gen;
