@@ -48,7 +48,7 @@ DevSell sell_view(const qsg_op* op, bool use_codes) {
   v.n_rows = static_cast<int>(op->n_rows);
   v.n_cols = static_cast<int>(op->n_cols);
   v.nnz = op->nnz;
-  v.code_bytes = use_codes ? op->code_bytes : 0;
+  v.code_bytes = (use_codes || op->col == nullptr) ? op->code_bytes : 0;  // coded-only ops decode
   v.code_off = op->code_off;
   v.code8 = op->code_bytes == 1 ? static_cast<const unsigned char*>(op->code) : nullptr;
   v.code16 = op->code_bytes == 2 ? static_cast<const unsigned short*>(op->code) : nullptr;
@@ -1005,12 +1005,30 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
     t_last = now;
   };
   // stage the CSR in HBM
+  // stage the CSR in HBM; input already in this device's memory (e.g. the device-assembled
+  // Liouvillian) is read in place instead of copied
   DevBuf d_rp, d_col, d_val, d_w;
-  if ((e = upload(d_rp, a->rowptr, sizeof(int) * (n + 1), s)) ||
-      (e = upload(d_col, a->col, sizeof(int) * a->nnz, s)) ||
-      (e = upload(d_val, a->val, sizeof(double2) * a->nnz, s)) ||
+  auto stage = [&](DevBuf& b, const void* src, size_t bytes, const void** p) -> cudaError_t {
+    cudaPointerAttributes pa;
+    if (src && cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeDevice &&
+        pa.device == ctx->device) {
+      *p = src;
+      return cudaSuccess;
+    }
+    cudaGetLastError();
+    const cudaError_t ue = upload(b, src, bytes, s);
+    *p = b.p;
+    return ue;
+  };
+  const void *prp = nullptr, *pcol = nullptr, *pval = nullptr;
+  if ((e = stage(d_rp, a->rowptr, sizeof(int) * (n + 1), &prp)) ||
+      (e = stage(d_col, a->col, sizeof(int) * a->nnz, &pcol)) ||
+      (e = stage(d_val, a->val, sizeof(double2) * a->nnz, &pval)) ||
       (e = d_w.alloc(sizeof(long long) * nsl, s)))
     return cuda_fail(e, "operator staging");
+  const int* srp = static_cast<const int*>(prp);
+  const int* scol = static_cast<const int*>(pcol);
+  const double2* sval = static_cast<const double2*>(pval);
   mark("upload");
   auto* op = new qsg_op;
   op->ctx = ctx;
@@ -1024,7 +1042,7 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
     qsg_op_destroy(op);
     return cuda_fail(e, "operator store allocation");
   }
-  sell_widths_kernel<<<static_cast<unsigned>((nsl * 32 + 255) / 256), 256, 0, s>>>(d_rp.as<int>(), static_cast<int>(n),
+  sell_widths_kernel<<<static_cast<unsigned>((nsl * 32 + 255) / 256), 256, 0, s>>>(srp, static_cast<int>(n),
                                                                             op->rowlen, d_w.as<long long>());
   std::vector<long long> w(nsl), off(nsl + 1, 0);
   if ((e = cudaMemcpyAsync(w.data(), d_w.p, sizeof(long long) * nsl, cudaMemcpyDeviceToHost, s)) ||
@@ -1038,43 +1056,50 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
     op->max_rowlen = std::max<int>(op->max_rowlen, static_cast<int>(w[i]));
   }
   op->padded_cols = off[nsl];
-  const size_t pe = static_cast<size_t>(std::max<long long>(1, off[nsl] * 32));
-  if ((e = cudaMallocAsync(&op->col, sizeof(int) * pe, s)) || (e = cudaMallocAsync(&op->val, sizeof(double2) * pe, s))) {
-    qsg_op_destroy(op);
-    return cuda_fail(e, "operator store allocation");
-  }
-  mark("alloc");
-  cudaMemsetAsync(op->col, 0, sizeof(int) * pe, s);
-  cudaMemsetAsync(op->val, 0, sizeof(double2) * pe, s);
-  mark("memset");
   cudaMemcpyAsync(op->slice_off, off.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, s);
   mark("slice_off");
-  sell_fill_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-      d_rp.as<int>(), d_col.as<int>(), d_val.as<double2>(), static_cast<int>(n), op->slice_off, op->col, op->val);
-  if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(s))) {
-    qsg_op_destroy(op);
-    return cuda_fail(e, "operator store build");
-  }
-  mark("sell fill");
   // Dictionary-coded store when the operator streams from HBM (otherwise it is L2-resident and
   // the code -> dictionary indirection only adds latency) and has <= 65535 distinct
-  // (diagonal offset, value) pairs. The plain entries stay resident too: the batched engine
-  // reads them. QSG_NO_COMPRESS=1 disables, QSG_COMPRESS_MIN_BYTES moves the size threshold.
+  // (diagonal offset, value) pairs. QSG_NO_COMPRESS=1 disables, QSG_COMPRESS_MIN_BYTES moves the
+  // size threshold.
   const char* nc = std::getenv("QSG_NO_COMPRESS");
   long long min_bytes = 32LL << 20;
   if (const char* mb = std::getenv("QSG_COMPRESS_MIN_BYTES")) min_bytes = std::atoll(mb);
   if (!(nc && nc[0] == '1') && a->nnz > 0 && 20 * a->nnz >= min_bytes) {
-    if ((e = build_coded_store(op, d_rp.as<int>(), d_col.as<int>(), d_val.as<double2>(), n, w, s))) {
+    if ((e = build_coded_store(op, srp, scol, sval, n, w, s))) {
       qsg_op_destroy(op);
       return cuda_fail(e, "coded operator store");
     }
     mark("coded");
   }
+  // The plain SELL entries, unless the coded store replaces them: every reader of a coded operator
+  // (grid engine, generator apply, batch engine via sell_view) then decodes the codes, and the
+  // e2e path saves the plain fill and ~20 B per entry of HBM (TFIM-10: 497 MB). QSG_KEEP_PLAIN=1
+  // builds both.
+  const char* kp = std::getenv("QSG_KEEP_PLAIN");
+  if (op->code_bytes == 0 || (kp && kp[0] == '1')) {
+    const size_t pe = static_cast<size_t>(std::max<long long>(1, off[nsl] * 32));
+    if ((e = cudaMallocAsync(&op->col, sizeof(int) * pe, s)) || (e = cudaMallocAsync(&op->val, sizeof(double2) * pe, s))) {
+      qsg_op_destroy(op);
+      return cuda_fail(e, "operator store allocation");
+    }
+    mark("alloc");
+    cudaMemsetAsync(op->col, 0, sizeof(int) * pe, s);
+    cudaMemsetAsync(op->val, 0, sizeof(double2) * pe, s);
+    mark("memset");
+    sell_fill_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+        srp, scol, sval, static_cast<int>(n), op->slice_off, op->col, op->val);
+    if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(s))) {
+      qsg_op_destroy(op);
+      return cuda_fail(e, "operator store build");
+    }
+    mark("sell fill");
+  }
   // key-aligned store, built on request (QSG_KA_STORE=1, or QSG_KA_SOLVE=1 for the grid solver)
   const char* kst = std::getenv("QSG_KA_STORE");
   const char* ksv = std::getenv("QSG_KA_SOLVE");
   if (a->nnz > 0 && ((kst && kst[0] == '1') || (ksv && ksv[0] == '1'))) {
-    if ((e = build_ka_store(op, d_rp.as<int>(), d_col.as<int>(), d_val.as<double2>(), n, s))) {
+    if ((e = build_ka_store(op, srp, scol, sval, n, s))) {
       qsg_op_destroy(op);
       return cuda_fail(e, "key-aligned operator store");
     }
