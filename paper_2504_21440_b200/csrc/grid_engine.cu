@@ -15,6 +15,7 @@
 //
 // Passes per attempt: 6 (stage 2 gathers y + h*a21*k1 on the fly), one grid barrier each.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 
 #include "engine.cuh"
@@ -897,8 +898,15 @@ __device__ __forceinline__ unsigned cl_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
+// Cluster barrier. Every value one CTA reads from another lives in shared memory, so the release
+// side only has to order this CTA's shared-memory writes: a shared::cta-restricted release fence
+// (MEMBAR.CTA + FENCE.VIEW.ASYNC.S) ahead of a relaxed arrive, instead of the MEMBAR.ALL.GPU that
+// `arrive.release` emits (-0.8 us per Kerr attempt, profiles/r02_cl_release.log); the wait keeps
+// its cluster-scope acquire.
 __device__ __forceinline__ void cl_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile(
+      "fence.release.sync_restrict::shared::cta.cluster;\n\t"
+      "barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ unsigned cl_map(unsigned saddr, unsigned rank) {
   unsigned r;
@@ -917,17 +925,19 @@ __device__ __forceinline__ double cl_ld(unsigned a) {
 }
 
 // element c (global index) of logical buffer b, from its owner CTA
-__device__ __forceinline__ double2 cl_elem(double2* const* p, int b, int c, int R) {
-  const unsigned owner = static_cast<unsigned>(c / R);
+// owner = c / R by a multiply-high with rmagic = ceil(2^32 / R): exact for c * R < 2^32, which the
+// plan guarantees (n <= 16 R, R < 2^14)
+__device__ __forceinline__ double2 cl_elem(double2* const* p, int b, int c, int R, unsigned rmagic) {
+  const unsigned owner = __umulhi(static_cast<unsigned>(c), rmagic);
   const unsigned loc = static_cast<unsigned>(c - static_cast<int>(owner) * R);
   return cl_ld2(cl_map(smem_u32(p[b] + loc), owner));
 }
 // dense output (integrator.hpp:127-131,150-154) at global index c, read from its owner CTA
-__device__ __forceinline__ double2 cl_dense(double2* const* p, int c, double theta, double h, int R) {
-  if (isnan(theta)) return cl_elem(p, Y, c, R);
-  const double2 yo = cl_elem(p, YO, c, R), y1 = cl_elem(p, Y, c, R), k1 = cl_elem(p, K7, c, R),
-                k7 = cl_elem(p, K1, c, R), k3 = cl_elem(p, K3, c, R), k4 = cl_elem(p, K4, c, R),
-                k5 = cl_elem(p, K5, c, R), k6 = cl_elem(p, K6, c, R);
+__device__ __forceinline__ double2 cl_dense(double2* const* p, int c, double theta, double h, int R, unsigned rm) {
+  if (isnan(theta)) return cl_elem(p, Y, c, R, rm);
+  const double2 yo = cl_elem(p, YO, c, R, rm), y1 = cl_elem(p, Y, c, R, rm), k1 = cl_elem(p, K7, c, R, rm),
+                k7 = cl_elem(p, K1, c, R, rm), k3 = cl_elem(p, K3, c, R, rm), k4 = cl_elem(p, K4, c, R, rm),
+                k5 = cl_elem(p, K5, c, R, rm), k6 = cl_elem(p, K6, c, R, rm);
   using namespace dp;
   const double th1 = 1.0 - theta;
   const double2 rc2 = csub(y1, yo);
@@ -957,12 +967,11 @@ __device__ __forceinline__ double cl_warp_sum(double* red, int k, int C) {
 // One SpMV row of the CTA's resident operator slice sl (lane = row in slice), gathering logical
 // buffer xb (S2: y + h a21 k1 on the fly) from every CTA's shared memory.
 template <bool S2>
-__device__ __forceinline__ double2 cl_row(const int* rowlen, const int* soff, const unsigned* tgt, const double2* val,
-                                          int sl, int lane, double2* const* p, int xb, double hh) {
+__device__ __forceinline__ double2 cl_row_at(const int* rowlen, const int* soff, const unsigned* tgt,
+                                             const double2* val, int sl, int lane, unsigned xa, unsigned ya,
+                                             unsigned ka, double hh) {
   const int len = rowlen[sl * 32 + lane];
   const int base = soff[sl] * 32 + lane;
-  const unsigned xa = smem_u32(p[xb]);
-  const unsigned ya = smem_u32(p[Y]), ka = smem_u32(p[K1]);
   double2 acc = make_double2(0.0, 0.0);
   constexpr int U = 8;  // one round of DSMEM gathers for rows of up to 8 entries (Kerr: 6)
   for (int j = 0; j < len; j += U) {
@@ -993,21 +1002,26 @@ __device__ __forceinline__ double2 cl_row(const int* rowlen, const int* soff, co
   }
   return acc;
 }
+template <bool S2>
+__device__ __forceinline__ double2 cl_row(const int* rowlen, const int* soff, const unsigned* tgt, const double2* val,
+                                          int sl, int lane, double2* const* p, int xb, double hh) {
+  return cl_row_at<S2>(rowlen, soff, tgt, val, sl, lane, smem_u32(p[xb]), smem_u32(p[Y]), smem_u32(p[K1]), hh);
+}
 
 #ifdef QSG_CL_TIMING
 __device__ unsigned long long g_cl_ns[16];
-__device__ __forceinline__ unsigned long long cl_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
+__device__ __forceinline__ unsigned long long cl_now() {  // SM clock cycles (globaltimer is too coarse)
+  return static_cast<unsigned long long>(clock64());
 }
-#define CL_T(k)                                                  \
-  do {                                                           \
-    if (rank == 0 && threadIdx.x == 0) {                         \
-      const unsigned long long _t = cl_now();                    \
-      g_cl_ns[k] += _t - cl_t_last;                              \
-      cl_t_last = _t;                                            \
-    }                                                            \
+// per-phase globaltimer deltas of CTA 0 thread 0, kept in registers until the kernel ends (a global
+// read-modify-write per phase would stall the timed thread and charge the stall to the next phase)
+#define CL_T(k)                               \
+  do {                                        \
+    if (rank == 0 && threadIdx.x == 0) {      \
+      const unsigned long long _t = cl_now(); \
+      cl_acc[k] += _t - cl_t_last;            \
+      cl_t_last = _t;                         \
+    }                                         \
   } while (0)
 #else
 #define CL_T(k) \
@@ -1034,6 +1048,9 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
   double2* val = reinterpret_cast<double2*>(s_dyn + L.val);
   double* red = reinterpret_cast<double*>(s_dyn + L.red);  // [0..3] control sums, [4..] observations
   const int kcap = max(1, min(kMaxPending, kObsSlots / (2 * max(1, P.n_e))));
+#ifdef QSG_CL_TIMING
+  unsigned long long cl_t_last = 0, cl_acc[12] = {};
+#endif
 
   // ---- prologue: the CTA's operator slices into shared memory (columns pre-split by owner) and
   // y0 rows; every other buffer starts uninitialised like the grid engine's
@@ -1145,7 +1162,8 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
         if (MODE == 0) {
           for (int k = eo_off[e] + gt; k < eo_off[e + 1]; k += gs) {
             const int i = eo_i[k], j = eo_j[k];
-            const double2 rji = cl_dense(p, i * P.d + j, th, hl, R), rij = cl_dense(p, j * P.d + i, th, hl, R);
+            const double2 rji = cl_dense(p, i * P.d + j, th, hl, R, L.rmagic),
+                          rij = cl_dense(p, j * P.d + i, th, hl, R, L.rmagic);
             acc[v] = cadd(acc[v], cmul(eo_v[k], cscale(0.5, cadd(rji, cconj(rij)))));
           }
         } else {
@@ -1154,11 +1172,12 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
           for (int r = r0 + threadIdx.x; r < r1; r += kClThreads) {
             double2 ev = make_double2(0.0, 0.0);
             for (int k = rp[r]; k < rp[r + 1]; ++k)
-              ev = cadd(ev, cmul(P.se_val[off + k], cl_dense(p, P.se_col[off + k], th, hl, R)));
-            acc[v] = cadd(acc[v], cmul(cconj(cl_dense(p, r, th, hl, R)), ev));
+              ev = cadd(ev, cmul(P.se_val[off + k], cl_dense(p, P.se_col[off + k], th, hl, R, L.rmagic)));
+            acc[v] = cadd(acc[v], cmul(cconj(cl_dense(p, r, th, hl, R, L.rmagic)), ev));
           }
         }
       }
+      CL_T(7);
       // one block reduction for all 2 kV values: warp shuffles, one smem row per warp, warp 0
       // folds the warps in order (the same order in every CTA)
       __shared__ double s_obs[kClThreads / 32][2 * kV];
@@ -1177,6 +1196,7 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
         bank[2 * b0 + lane] = t;
       }
       __syncthreads();
+      CL_T(8);
     }
     for (int q = 0; q < np; ++q) {
       if (c.pend[q].save_idx < 0) continue;
@@ -1185,9 +1205,9 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
       for (int r = r0 + threadIdx.x; r < r1; r += kClThreads) {
         if (MODE == 0) {
           const int i = r % P.d, j = r / P.d;
-          out[r] = cscale(0.5, cadd(cl_dense(p, r, th, hl, R), cconj(cl_dense(p, i * P.d + j, th, hl, R))));
+          out[r] = cscale(0.5, cadd(cl_dense(p, r, th, hl, R, L.rmagic), cconj(cl_dense(p, i * P.d + j, th, hl, R, L.rmagic))));
         } else {
-          out[r] = cl_dense(p, r, th, hl, R);
+          out[r] = cl_dense(p, r, th, hl, R, L.rmagic);
         }
       }
     }
@@ -1305,7 +1325,6 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
   // ---- solve loop (evolve.cpp:156-167)
   using namespace dp;
 #ifdef QSG_CL_TIMING
-  unsigned long long cl_t_last = 0;
   if (rank == 0 && threadIdx.x == 0) cl_t_last = cl_now();
 #endif
   for (;;) {
@@ -1406,6 +1425,10 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
     // the six stage barriers in between order that
     if (c.done) break;
   }
+#ifdef QSG_CL_TIMING
+  if (rank == 0 && threadIdx.x == 0)
+    for (int k = 0; k < 12; ++k) g_cl_ns[k] += cl_acc[k];
+#endif
   if (c.status == kRunning) {
     if (c.np) flush();
     while (c.next < P.n_ev) {
@@ -1556,6 +1579,8 @@ bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, i
     L.R = R;
     L.S = S;
     L.E = static_cast<int>(E);
+    if (R >= (1 << 14)) break;  // cl_elem's multiply-high division needs R < 2^14 (n <= 16 R)
+    L.rmagic = static_cast<unsigned>(((1ull << 32) + R - 1) / R);
     unsigned o = 0;
     L.vec = o;
     o = al(o + 11u * R * 16u);

@@ -21,7 +21,8 @@ L.qsg_debug_cluster_ns(buf, 1)
 r = q.mesolve(ctx, g, m.dim, rho0, tl, eops)
 L.qsg_debug_cluster_ns(buf, 1)
 att = r["attempts"]
-names = ["begin+sync", "stage SpMV+epilogue", "observe", "block_sum+cl_sync", "obs commit", "finish_attempt", "flush"]
+names = ["begin+sync", "stage SpMV+epilogue", "observe (saves)", "block_sum+cl_sync", "obs commit", "finish_attempt", "flush", "observe items", "observe reduce"]
+CLK_GHZ = float(os.environ.get("CLK_GHZ", "1.965"))  # cl_now() counts SM cycles
 print("N", N, "attempts", att, "kernel_ms", r["kernel_ms"], "us/attempt", r["kernel_ms"] * 1e3 / att)
 for i, nm in enumerate(names):
-    print(f"{nm:24s} {buf[i] / att / 1e3:8.3f} us/attempt")
+    print(f"{nm:24s} {buf[i] / att / CLK_GHZ / 1e3:8.3f} us/attempt")
