@@ -891,7 +891,8 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
 // (Ctl, begin_attempt, finish_attempt), replicated identically in every CTA; reductions are CTA
 // partials read by every CTA from every CTA's shared memory in rank order (deterministic).
 constexpr int kClThreads = 512;
-constexpr int kEvSmem = 1024;  // events staged in shared memory when the solve has at most this many
+constexpr int kEvSmem = 1024;
+constexpr int kObsDirectMax = 4096;  // mesolve e_op entries up to which CTA 0 observes alone  // events staged in shared memory when the solve has at most this many
 
 __device__ __forceinline__ unsigned cl_rank() {
   unsigned r;
@@ -1140,6 +1141,11 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
   // bank of observation slots in red[] (double-buffered by c.obs_par, like the grid engine's):
   // a bank is rewritten two observation events later, after at least one more cluster barrier
   auto obs_bank = [&](int par) { return red + 4 + par * kObsSlots; };
+  // mesolve with few e_op entries: CTA 0 forms the expectation values alone and writes them, so
+  // an observation needs no cluster-wide partial sums and no commit after the barrier (the other
+  // CTAs' buffers it reads are not rewritten before the next stage-2 barrier, which CTA 0 joins
+  // only after observing)
+  const bool obs_direct = MODE == 0 && L.obs_direct;
   auto observe = [&]() {
     double2* const* p = c.p;
     const int np = c.np;
@@ -1152,8 +1158,49 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
       double2 acc[kV];
 #pragma unroll
       for (int v = 0; v < kV; ++v) acc[v] = make_double2(0.0, 0.0);
+      if (obs_direct) {
+        // CTA 0 alone: the kV pairs' e_op entries as one flat list over its threads (every pair's
+        // dense-output gathers in flight together); its block sum is the expectation value
+        if (rank != 0) break;
+        int pre[kV + 1], eb[kV];
+        double thv[kV];
+        pre[0] = 0;
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+          const int pr = b0 + v;
+          int cnt = 0;
+          eb[v] = 0;
+          thv[v] = 0.0;
+          if (pr < npairs) {
+            const int q = pr / P.n_e, e = pr % P.n_e;
+            if (c.pend[q].grid_idx >= 0) {
+              eb[v] = eo_off[e];
+              cnt = eo_off[e + 1] - eo_off[e];
+              thv[v] = c.pend[q].theta;
+            }
+          }
+          pre[v + 1] = pre[v] + cnt;
+        }
+        for (int i = threadIdx.x; i < pre[kV]; i += kClThreads) {
+          int k = 0;
+          double th = 0.0;
+#pragma unroll
+          for (int v = 0; v < kV; ++v)
+            if (i >= pre[v] && i < pre[v + 1]) {
+              k = eb[v] + (i - pre[v]);
+              th = thv[v];
+            }
+          const int ei = eo_i[k], ej = eo_j[k];
+          const double2 x = cmul(eo_v[k], cscale(0.5, cadd(cl_dense(p, ei * P.d + ej, th, hl, R, L.rmagic),
+                                                             cconj(cl_dense(p, ej * P.d + ei, th, hl, R, L.rmagic)))));
+#pragma unroll
+          for (int v = 0; v < kV; ++v)
+            if (i >= pre[v] && i < pre[v + 1]) acc[v] = cadd(acc[v], x);
+        }
+      }
 #pragma unroll
       for (int v = 0; v < kV; ++v) {
+        if (obs_direct) break;
         const int pr = b0 + v;
         if (pr >= npairs) break;
         const int q = pr / P.n_e, e = pr % P.n_e;
@@ -1193,7 +1240,13 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
       if (warp == 0 && lane < 2 * kV && b0 + lane / 2 < npairs) {
         double t = 0.0;
         for (int w = 0; w < W; ++w) t += s_obs[w][lane];
-        bank[2 * b0 + lane] = t;
+        if (obs_direct) {
+          const int pr = b0 + lane / 2, q = pr / P.n_e, e = pr % P.n_e;
+          if (c.pend[q].grid_idx >= 0)
+            reinterpret_cast<double*>(P.expect + static_cast<long long>(c.pend[q].grid_idx) * P.n_e + e)[lane & 1] = t;
+        } else {
+          bank[2 * b0 + lane] = t;
+        }
       }
       __syncthreads();
       CL_T(8);
@@ -1226,8 +1279,10 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
   };
   auto flush = [&]() {
     observe();
-    cl_sync();
-    observe_commit_cl();
+    if (!obs_direct) {
+      cl_sync();
+      observe_commit_cl();
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
       c.np = 0;
@@ -1258,7 +1313,7 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
     }
     if (c.np) observe();
     cl_sync();
-    if (c.np) observe_commit_cl();
+    if (c.np && !obs_direct) observe_commit_cl();
     __shared__ double s_tot[3];
     if (warp == 0) {
       const double t0 = cl_warp_sum(red, 0, C), t1 = cl_warp_sum(red, 1, C);
@@ -1336,6 +1391,7 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
     CL_T(0);
     if (c.done || c.status != kRunning) break;
     const double hh = c.hh, t = c.t;
+    const int np_s = c.np;  // pending observations of the previous step (every thread, one read)
     (void)t;
     // stage passes 2..7 (integrator.hpp:91-102) on local rows, gathers from the cluster
     for (int S = 2; S <= 7; ++S) {
@@ -1384,7 +1440,7 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
         }
       }
       CL_T(1);
-      if (S == 2 && c.np) observe();  // the previous step's events, on the buffers of that step
+      if (S == 2 && np_s) observe();  // the previous step's events, on the buffers of that step
       CL_T(2);
       if (S == 7) {
         esq = block_sum(esq, s_red);
@@ -1392,14 +1448,15 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
       }
       cl_sync();
       CL_T(3);
-      if (S == 2 && c.np) {
-        observe_commit_cl();
-        __syncthreads();
-        if (threadIdx.x == 0) {
+      if (S == 2 && np_s) {
+        if (!obs_direct) {
+          observe_commit_cl();
+          __syncthreads();
+        }
+        if (threadIdx.x == 0) {  // c.np is next read after the controller's block barrier
           c.np = 0;
           c.obs_par ^= 1;
         }
-        __syncthreads();
       }
       CL_T(4);
     }
@@ -1606,6 +1663,8 @@ bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, i
       L.n_eo = n_eo;
       L.bytes = o + eo_bytes;
     }
+    L.obs_direct = n_eo <= kObsDirectMax ? 1 : 0;
+    if (const char* od = std::getenv("QSG_CL_OBS_DIRECT")) L.obs_direct = od[0] == '0' ? 0 : L.obs_direct;
     // the smallest cluster whose per-CTA share fits (more CTAs only add DSMEM hops and barrier
     // arrivals); 16 slices per CTA at most so every warp owns at most one slice per pass
     if (L.bytes + static_smem <= 226u * 1024u && S <= 64 && R < (1 << 24)) {  // 227 KB per CTA at most
