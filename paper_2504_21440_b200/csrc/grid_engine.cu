@@ -891,8 +891,7 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
 // (Ctl, begin_attempt, finish_attempt), replicated identically in every CTA; reductions are CTA
 // partials read by every CTA from every CTA's shared memory in rank order (deterministic).
 constexpr int kClThreads = 512;
-constexpr int kEvSmem = 1024;
-constexpr int kObsDirectMax = 4096;  // mesolve e_op entries up to which CTA 0 observes alone  // events staged in shared memory when the solve has at most this many
+constexpr int kEvSmem = 1024;  // events staged in shared memory when the solve has at most this many
 
 __device__ __forceinline__ unsigned cl_rank() {
   unsigned r;
@@ -1050,7 +1049,7 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
   double* red = reinterpret_cast<double*>(s_dyn + L.red);  // [0..3] control sums, [4..] observations
   const int kcap = max(1, min(kMaxPending, kObsSlots / (2 * max(1, P.n_e))));
 #ifdef QSG_CL_TIMING
-  unsigned long long cl_t_last = 0, cl_acc[12] = {};
+  unsigned long long cl_t_last = cl_now(), cl_acc[12] = {};
 #endif
 
   // ---- prologue: the CTA's operator slices into shared memory (columns pre-split by owner) and
@@ -1141,27 +1140,28 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
   // bank of observation slots in red[] (double-buffered by c.obs_par, like the grid engine's):
   // a bank is rewritten two observation events later, after at least one more cluster barrier
   auto obs_bank = [&](int par) { return red + 4 + par * kObsSlots; };
-  // mesolve with few e_op entries: CTA 0 forms the expectation values alone and writes them, so
-  // an observation needs no cluster-wide partial sums and no commit after the barrier (the other
-  // CTAs' buffers it reads are not rewritten before the next stage-2 barrier, which CTA 0 joins
-  // only after observing)
-  const bool obs_direct = MODE == 0 && L.obs_direct;
-  auto observe = [&]() {
+  // ow: one warp (the caller, lane = item index) does the whole observation with no block barrier,
+  // so it can run beside the other warps' stage-2 pass (MODE 0 only)
+  auto observe = [&](bool ow = false) {
+    const int tid = ow ? lane : static_cast<int>(threadIdx.x), nthr = ow ? 32 : kClThreads;
     double2* const* p = c.p;
     const int np = c.np;
     const double hl = c.h_last;
-    const int gt = rank * kClThreads + threadIdx.x, gs = C * kClThreads;
     double* bank = obs_bank(c.obs_par);
     const int npairs = np * P.n_e;
-    constexpr int kV = 8;  // (event, e_op) pairs reduced together
+    // (event, e_op) pairs reduced together: 2, because every extra pair's unrolled reduction grows
+    // the per-event code, and that code plus the per-attempt loop must fit the SM's instruction
+    // cache (kV 8 -> 2: Kerr-20 10.8 -> 9.9 us per attempt, profiles/r02_cl_kv.log)
+    constexpr int kV = 2;
     for (int b0 = 0; b0 < npairs; b0 += kV) {
+      const int nv = min(kV, npairs - b0);
       double2 acc[kV];
 #pragma unroll
       for (int v = 0; v < kV; ++v) acc[v] = make_double2(0.0, 0.0);
-      if (obs_direct) {
-        // CTA 0 alone: the kV pairs' e_op entries as one flat list over its threads (every pair's
-        // dense-output gathers in flight together); its block sum is the expectation value
-        if (rank != 0) break;
+      int tl;  // this CTA's work items (threads with work: the first tl)
+      if (MODE == 0) {
+        // the pairs' e_op entries as one flat list, item i on CTA i % C: every CTA's DSMEM port
+        // carries a share of the dense-output gathers and every pair is in flight at once
         int pre[kV + 1], eb[kV];
         double thv[kV];
         pre[0] = 0;
@@ -1171,7 +1171,7 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
           int cnt = 0;
           eb[v] = 0;
           thv[v] = 0.0;
-          if (pr < npairs) {
+          if (v < nv) {
             const int q = pr / P.n_e, e = pr % P.n_e;
             if (c.pend[q].grid_idx >= 0) {
               eb[v] = eo_off[e];
@@ -1181,7 +1181,9 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
           }
           pre[v + 1] = pre[v] + cnt;
         }
-        for (int i = threadIdx.x; i < pre[kV]; i += kClThreads) {
+        tl = (pre[kV] - rank + C - 1) / C;
+        for (int il = tid; il < tl; il += nthr) {
+          const int i = il * C + rank;
           int k = 0;
           double th = 0.0;
 #pragma unroll
@@ -1197,26 +1199,18 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
           for (int v = 0; v < kV; ++v)
             if (i >= pre[v] && i < pre[v + 1]) acc[v] = cadd(acc[v], x);
         }
-      }
+      } else {
+        tl = r1 - r0;
 #pragma unroll
-      for (int v = 0; v < kV; ++v) {
-        if (obs_direct) break;
-        const int pr = b0 + v;
-        if (pr >= npairs) break;
-        const int q = pr / P.n_e, e = pr % P.n_e;
-        const double th = c.pend[q].theta;
-        if (c.pend[q].grid_idx < 0) continue;
-        if (MODE == 0) {
-          for (int k = eo_off[e] + gt; k < eo_off[e + 1]; k += gs) {
-            const int i = eo_i[k], j = eo_j[k];
-            const double2 rji = cl_dense(p, i * P.d + j, th, hl, R, L.rmagic),
-                          rij = cl_dense(p, j * P.d + i, th, hl, R, L.rmagic);
-            acc[v] = cadd(acc[v], cmul(eo_v[k], cscale(0.5, cadd(rji, cconj(rij)))));
-          }
-        } else {
+        for (int v = 0; v < kV; ++v) {
+          if (v >= nv) break;
+          const int pr = b0 + v;
+          const int q = pr / P.n_e, e = pr % P.n_e;
+          const double th = c.pend[q].theta;
+          if (c.pend[q].grid_idx < 0) continue;
           const int* rp = P.se_rowptr + static_cast<long long>(e) * (P.n + 1);
           const long long off = P.se_off[e];
-          for (int r = r0 + threadIdx.x; r < r1; r += kClThreads) {
+          for (int r = r0 + tid; r < r1; r += nthr) {
             double2 ev = make_double2(0.0, 0.0);
             for (int k = rp[r]; k < rp[r + 1]; ++k)
               ev = cadd(ev, cmul(P.se_val[off + k], cl_dense(p, P.se_col[off + k], th, hl, R, L.rmagic)));
@@ -1225,37 +1219,47 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
         }
       }
       CL_T(7);
-      // one block reduction for all 2 kV values: warp shuffles, one smem row per warp, warp 0
-      // folds the warps in order (the same order in every CTA)
-      __shared__ double s_obs[kClThreads / 32][2 * kV];
+      // the CTA's partial of each of the 2 nv values, in a fixed order: warp shuffles, then (more
+      // than one warp with work) one smem row per warp folded by warp 0
+      const int aw = min(W, (tl + 31) >> 5);  // warps with work (uniform in the CTA)
+      if (ow || aw <= 1) {
+        if (ow || warp == 0)
 #pragma unroll
-      for (int v = 0; v < kV; ++v) {
-        const double x = warp_sum(acc[v].x), y = warp_sum(acc[v].y);
-        if (lane == 0) {
-          s_obs[warp][2 * v] = x;
-          s_obs[warp][2 * v + 1] = y;
-        }
-      }
-      __syncthreads();
-      if (warp == 0 && lane < 2 * kV && b0 + lane / 2 < npairs) {
-        double t = 0.0;
-        for (int w = 0; w < W; ++w) t += s_obs[w][lane];
-        if (obs_direct) {
-          const int pr = b0 + lane / 2, q = pr / P.n_e, e = pr % P.n_e;
-          if (c.pend[q].grid_idx >= 0)
-            reinterpret_cast<double*>(P.expect + static_cast<long long>(c.pend[q].grid_idx) * P.n_e + e)[lane & 1] = t;
-        } else {
+          for (int v = 0; v < kV; ++v) {
+            if (v >= nv) break;
+            const double x = warp_sum(acc[v].x), y = warp_sum(acc[v].y);
+            if (lane == 0) {
+              bank[2 * (b0 + v)] = x;
+              bank[2 * (b0 + v) + 1] = y;
+            }
+          }
+      } else {
+        __shared__ double s_obs[kClThreads / 32][2 * kV];
+        if (warp < aw)
+#pragma unroll
+          for (int v = 0; v < kV; ++v) {
+            if (v >= nv) break;
+            const double x = warp_sum(acc[v].x), y = warp_sum(acc[v].y);
+            if (lane == 0) {
+              s_obs[warp][2 * v] = x;
+              s_obs[warp][2 * v + 1] = y;
+            }
+          }
+        __syncthreads();
+        if (warp == 0 && lane < 2 * nv) {
+          double t = 0.0;
+          for (int w = 0; w < aw; ++w) t += s_obs[w][lane];
           bank[2 * b0 + lane] = t;
         }
+        __syncthreads();
       }
-      __syncthreads();
       CL_T(8);
     }
     for (int q = 0; q < np; ++q) {
       if (c.pend[q].save_idx < 0) continue;
       const double th = c.pend[q].theta;
       double2* out = P.states + static_cast<long long>(c.pend[q].save_idx) * P.n;
-      for (int r = r0 + threadIdx.x; r < r1; r += kClThreads) {
+      for (int r = r0 + tid; r < r1; r += nthr) {
         if (MODE == 0) {
           const int i = r % P.d, j = r / P.d;
           out[r] = cscale(0.5, cadd(cl_dense(p, r, th, hl, R, L.rmagic), cconj(cl_dense(p, i * P.d + j, th, hl, R, L.rmagic))));
@@ -1265,24 +1269,27 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
       }
     }
   };
-  // after the barrier that follows observe(): every CTA folds the partials; CTA 0 writes expect[]
-  auto observe_commit_cl = [&]() {
-    const int nv = 2 * c.np * P.n_e;
-    const int base = static_cast<int>(obs_bank(c.obs_par) - red);
-    if (rank == 0)
-      for (int s2 = warp; s2 < nv; s2 += W) {  // one warp per value: the C partials in flight at once
-        const double v = cl_warp_sum(red, base + s2, C);
-        const int q = (s2 / 2) / P.n_e, e = (s2 / 2) % P.n_e;
-        if (lane == 0 && c.pend[q].grid_idx >= 0)
-          reinterpret_cast<double*>(P.expect + static_cast<long long>(c.pend[q].grid_idx) * P.n_e + e)[s2 & 1] = v;
-      }
+  // after the barrier that follows observe(), in CTA 0: warps w0, w0 + ws, ... fold the C CTA
+  // partials of one value each (lane r reads CTA r) and write expect[]. np / par: the observation's
+  // pending count and bank parity (captured, since thread 0 may already be resetting them).
+  auto observe_commit_cl = [&](int np, int par, int w0, int ws) {
+    const int nv = 2 * np * P.n_e;
+    const int base = static_cast<int>(obs_bank(par) - red);
+    for (int s2 = w0; s2 < nv; s2 += ws) {
+      const double v = cl_warp_sum(red, base + s2, C);
+      const int q = (s2 / 2) / P.n_e, e = (s2 / 2) % P.n_e;
+      if (lane == 0 && c.pend[q].grid_idx >= 0)
+        reinterpret_cast<double*>(P.expect + static_cast<long long>(c.pend[q].grid_idx) * P.n_e + e)[s2 & 1] = v;
+    }
   };
+  // the stage-2 observation's commit: by CTA 0's last warp while the other warps run stage 3 when
+  // that warp owns no slice, else by all of CTA 0's warps before stage 3
+  const bool defer_commit = nsl <= W - 1;
+  const bool obs_ow = MODE == 0 && nsl <= W - 1 && L.obs_ow;
   auto flush = [&]() {
     observe();
-    if (!obs_direct) {
-      cl_sync();
-      observe_commit_cl();
-    }
+    cl_sync();
+    if (rank == 0) observe_commit_cl(c.np, c.obs_par, warp, W);
     __syncthreads();
     if (threadIdx.x == 0) {
       c.np = 0;
@@ -1313,7 +1320,7 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
     }
     if (c.np) observe();
     cl_sync();
-    if (c.np && !obs_direct) observe_commit_cl();
+    if (c.np && rank == 0) observe_commit_cl(c.np, c.obs_par, warp, W);
     __shared__ double s_tot[3];
     if (warp == 0) {
       const double t0 = cl_warp_sum(red, 0, C), t1 = cl_warp_sum(red, 1, C);
@@ -1391,7 +1398,7 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
     CL_T(0);
     if (c.done || c.status != kRunning) break;
     const double hh = c.hh, t = c.t;
-    const int np_s = c.np;  // pending observations of the previous step (every thread, one read)
+    const int np_s = c.np, par_s = c.obs_par;  // the previous step's pending observations
     (void)t;
     // stage passes 2..7 (integrator.hpp:91-102) on local rows, gathers from the cluster
     for (int S = 2; S <= 7; ++S) {
@@ -1440,7 +1447,12 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
         }
       }
       CL_T(1);
-      if (S == 2 && np_s) observe();  // the previous step's events, on the buffers of that step
+      // the previous step's events, on the buffers of that step: by the last warp beside the pass
+      // when it owns no slice (mesolve), else by the whole CTA after it
+      if (S == 2 && np_s) {
+        if (!obs_ow) observe();
+        else if (warp == W - 1) observe(true);
+      }
       CL_T(2);
       if (S == 7) {
         esq = block_sum(esq, s_red);
@@ -1449,9 +1461,13 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
       cl_sync();
       CL_T(3);
       if (S == 2 && np_s) {
-        if (!obs_direct) {
-          observe_commit_cl();
-          __syncthreads();
+        if (rank == 0) {
+          if (!defer_commit) {
+            observe_commit_cl(np_s, par_s, warp, W);
+            __syncthreads();
+          } else if (warp == W - 1) {
+            observe_commit_cl(np_s, par_s, 0, 1);
+          }
         }
         if (threadIdx.x == 0) {  // c.np is next read after the controller's block barrier
           c.np = 0;
@@ -1636,6 +1652,8 @@ bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, i
     L.R = R;
     L.S = S;
     L.E = static_cast<int>(E);
+    L.obs_ow = 1;
+    if (const char* ow = std::getenv("QSG_CL_OBS_WARP")) L.obs_ow = ow[0] != '0';
     if (R >= (1 << 14)) break;  // cl_elem's multiply-high division needs R < 2^14 (n <= 16 R)
     L.rmagic = static_cast<unsigned>(((1ull << 32) + R - 1) / R);
     unsigned o = 0;
@@ -1663,8 +1681,6 @@ bool plan_cluster_solve(const GridProblem& P, const long long* slice_off_host, i
       L.n_eo = n_eo;
       L.bytes = o + eo_bytes;
     }
-    L.obs_direct = n_eo <= kObsDirectMax ? 1 : 0;
-    if (const char* od = std::getenv("QSG_CL_OBS_DIRECT")) L.obs_direct = od[0] == '0' ? 0 : L.obs_direct;
     // the smallest cluster whose per-CTA share fits (more CTAs only add DSMEM hops and barrier
     // arrivals); 16 slices per CTA at most so every warp owns at most one slice per pass
     if (L.bytes + static_smem <= 226u * 1024u && S <= 64 && R < (1 << 24)) {  // 227 KB per CTA at most

@@ -61,7 +61,7 @@ struct ClLayout {
   int E;  // entry capacity (32 * the widest CTA's summed slice widths)
   int n_eo;  // mesolve e_op entries staged in shared memory (0: read from global)
   unsigned rmagic;  // ceil(2^32 / R): owner CTA of a row by multiply-high
-  int obs_direct;  // mesolve observations by CTA 0 alone (few e_op entries)
+  int obs_ow;  // stage-2 observation by one otherwise idle warp beside the pass
   unsigned vec, rowlen, soff, tgt, val, red, eo, bytes;
 };
 // true (and the cluster size / layout) when a single-term plain-store generator fits one cluster;
