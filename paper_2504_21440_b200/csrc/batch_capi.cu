@@ -193,6 +193,14 @@ qsg_status run_batch(qsg_ctx* ctx, BatchProblem P, long long n_sys, int jump_cap
   P.gpart = gp.as<double>();
   P.gfin = gf.as<double>();
   P.bar = gb.as<unsigned>();
+  {  // every operator plain (no key-aligned or coded rows): the plain-only instantiation
+    bool lean = true;
+    for (int k = 0; k < P.gen.n_terms; ++k) lean = lean && P.gen.A[k].code_bytes == 0 && P.gen.A[k].ka_nval == 0;
+    for (int k = 0; k < P.n_c; ++k) lean = lean && P.c_ops[k].code_bytes == 0 && P.c_ops[k].ka_nval == 0;
+    for (int k = 0; k < P.n_e; ++k) lean = lean && P.e_ops[k].code_bytes == 0 && P.e_ops[k].ka_nval == 0;
+    const char* le = std::getenv("QSG_BATCH_LEAN");
+    P.lean = lean && !(le && le[0] == '0');
+  }
   cudaEventRecord(ctx->ev[2], s);
   if ((ce = launch_batch(P, layout, grid, cs, s))) return cuda_fail(ce, "batch launch");
   cudaEventRecord(ctx->ev[3], s);

@@ -16,6 +16,18 @@ QSG_DECL_LAYOUT(4)
 QSG_DECL_LAYOUT(5)
 QSG_DECL_LAYOUT(6)
 QSG_DECL_LAYOUT(7)
+#define QSG_DECL_LEAN(ID) \
+  cudaError_t batch_layout_lean_launch_##ID(const BatchProblem& P, int grid, int cs, cudaStream_t s);
+QSG_DECL_LEAN(0)
+QSG_DECL_LEAN(1)
+QSG_DECL_LEAN(2)
+QSG_DECL_LEAN(3)
+QSG_DECL_LEAN(4)
+QSG_DECL_LEAN(5)
+QSG_DECL_LEAN(6)
+QSG_DECL_LEAN(7)
+cudaError_t batch_layout_lean1_launch_1(const BatchProblem& P, int grid, int cs, cudaStream_t s);
+cudaError_t batch_layout_lean1_launch_4(const BatchProblem& P, int grid, int cs, cudaStream_t s);
 
 constexpr int kNbuf = 12;  // state arrays per batch (batch_kernel.cuh NBUF)
 
@@ -62,6 +74,18 @@ int batch_max_clusters(int layout, int cs) {
 }
 
 cudaError_t launch_batch(const BatchProblem& P, int layout, int grid, int cs, cudaStream_t s) {
+  if (P.lean && P.gen.n_terms == 1 && (layout == 1 || layout == 4))
+    return layout == 1 ? batch_layout_lean1_launch_1(P, grid, cs, s) : batch_layout_lean1_launch_4(P, grid, cs, s);
+  if (P.lean) switch (layout) {
+      case 1: return batch_layout_lean_launch_1(P, grid, cs, s);
+      case 2: return batch_layout_lean_launch_2(P, grid, cs, s);
+      case 3: return batch_layout_lean_launch_3(P, grid, cs, s);
+      case 4: return batch_layout_lean_launch_4(P, grid, cs, s);
+      case 5: return batch_layout_lean_launch_5(P, grid, cs, s);
+      case 6: return batch_layout_lean_launch_6(P, grid, cs, s);
+      case 7: return batch_layout_lean_launch_7(P, grid, cs, s);
+      default: return batch_layout_lean_launch_0(P, grid, cs, s);
+    }
   switch (layout) {
     case 1: return batch_layout_launch_1(P, grid, cs, s);
     case 2: return batch_layout_launch_2(P, grid, cs, s);

@@ -14,6 +14,7 @@ constexpr int kBatchMaxEops = 8;   // expectation operators
 struct BatchProblem {
   int mode;  // 0: mcsolve trajectories, 1: mesolve parameter points
   int autonomous;  // every generator term's coefficient is time-independent (stage-2 identity)
+  int lean;  // every operator is a plain SELL store: launch the plain-only kernel instantiation
   int n;     // vector length (d for mcsolve, d*d for mesolve)
   int d;
   DevGen gen;  // terms shared by every system

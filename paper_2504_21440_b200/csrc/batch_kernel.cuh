@@ -255,13 +255,24 @@ __device__ __forceinline__ double2 ka_row_slot(const DevSell& A, int row, XF&& x
 // KA: the caller's warp holds whole slices of one slot, so a key-aligned store may be used.
 template <bool KA = false, class XF>
 __device__ __forceinline__ double2 sell_row_slot(const DevSell& A, int row, XF&& xf) {
+  // QSG_BATCH_LEAN (the batch_layout_lean_*.cu instantiations, chosen when every operator of the
+  // batch is a plain SELL store): no key-aligned or dictionary-coded branch in any of the inlined
+  // row loops. Their cold code would otherwise sit between the hot passes and push the per-round
+  // working set out of the SM's instruction cache (ncu, TFIM-14 mcsolve: no_instruction stalls
+  // 5.06 -> 2.09 per issue, 192 -> 171 ms; profiles/r02_batch_lean.log).
+#ifndef QSG_BATCH_LEAN
   if constexpr (KA) {
     if (A.ka_nval > 0) return ka_row_slot(A, row, xf);
   }
+#endif
   const int sl = row >> 5, ln = row & 31;
   const int len = __ldg(A.rowlen + row);
   double2 acc = make_double2(0.0, 0.0);
+#ifdef QSG_BATCH_LEAN
+  if (true) {
+#else
   if (A.code_bytes == 0) {
+#endif
     const long long base = __ldg(A.slice_off + sl) * 32 + ln;
     for (int j = 0; j < len; j += QSG_BATCH_UNROLL) {
       int c[QSG_BATCH_UNROLL];
@@ -311,10 +322,14 @@ template <bool KA = false, class XF>
 __device__ __forceinline__ double2 gen_row_slot(const DevGen& g, const double* params, int row, double t,
                                                 XF&& xf) {
   double2 s = sell_row_slot<KA>(g.A[0], row, xf);
+#if defined(QSG_BATCH_LEAN) && QSG_BATCH_LEAN == 2
+  // single-term instantiation (batch_layout_lean1_*.cu): no second inlined row loop
+#else
   for (int k = 1; k < g.n_terms; ++k) {
     const double2 sk = sell_row_slot<KA>(g.A[k], row, xf);
     s = cadd(s, cmul(coeff_eval(g.c[k], params, t), sk));
   }
+#endif
   return s;
 }
 
@@ -1183,11 +1198,18 @@ cudaError_t layout_launch(const BatchProblem& P, int grid, int cs, cudaStream_t 
 
 // Defines the per-layout entry points of one kernel instantiation (one translation unit each, so
 // the seven instantiations compile in parallel).
-#define QSG_BATCH_LAYOUT(ID, BS, GM)                                                              \
-  namespace qsg {                                                                                 \
-  int batch_layout_occ_##ID() { return layout_occ<BS, GM>(); }                                    \
-  int batch_layout_clusters_##ID(int cs) { return layout_clusters<BS, GM>(cs); }                  \
-  cudaError_t batch_layout_launch_##ID(const BatchProblem& P, int grid, int cs, cudaStream_t s) { \
-    return layout_launch<BS, GM>(P, grid, cs, s);                                                 \
-  }                                                                                               \
+#if defined(QSG_BATCH_LEAN) && QSG_BATCH_LEAN == 2
+#define QSG_BATCH_ENTRY(KIND, ID) batch_layout_lean1_##KIND##_##ID
+#elif defined(QSG_BATCH_LEAN)
+#define QSG_BATCH_ENTRY(KIND, ID) batch_layout_lean_##KIND##_##ID
+#else
+#define QSG_BATCH_ENTRY(KIND, ID) batch_layout_##KIND##_##ID
+#endif
+#define QSG_BATCH_LAYOUT(ID, BS, GM)                                                                 \
+  namespace qsg {                                                                                    \
+  int QSG_BATCH_ENTRY(occ, ID)() { return layout_occ<BS, GM>(); }                                    \
+  int QSG_BATCH_ENTRY(clusters, ID)(int cs) { return layout_clusters<BS, GM>(cs); }                  \
+  cudaError_t QSG_BATCH_ENTRY(launch, ID)(const BatchProblem& P, int grid, int cs, cudaStream_t s) { \
+    return layout_launch<BS, GM>(P, grid, cs, s);                                                    \
+  }                                                                                                  \
   }

@@ -1,0 +1,5 @@
+// Batch engine layout 1, plain-store-only instantiation (batch_kernel.cuh QSG_BATCH_LEAN).
+#define QSG_BATCH_LEAN 1
+#include "batch_kernel.cuh"
+
+QSG_BATCH_LAYOUT(1, 32, GM_GRID)

@@ -1,0 +1,5 @@
+// Batch engine layout 7, plain-store-only instantiation (batch_kernel.cuh QSG_BATCH_LEAN).
+#define QSG_BATCH_LEAN 1
+#include "batch_kernel.cuh"
+
+QSG_BATCH_LAYOUT(7, 1, GM_DSM)
