@@ -281,6 +281,7 @@ extern "C" qsg_status qsg_mcsolve(qsg_ctx* ctx, const qsg_generator* G, int32_t 
                                   const double* tlist, int64_t n_t, const double* params, int32_t n_params,
                                   uint64_t seed, int64_t traj_begin, int64_t traj_end, const qsg_solve_opts* opts,
                                   qsg_mc_out* out, qsg_timing* timing) {
+  QSG_RANGE("qsg_mcsolve");
   BatchProblem P{};
   if (qsg_status s = common_setup(ctx, G, d, tlist, n_t, opts, P)) return s;
   if (traj_end <= traj_begin) {
@@ -388,6 +389,7 @@ extern "C" qsg_status qsg_mesolve_batch(qsg_ctx* ctx, const qsg_generator* L, in
                                         int64_t n_points, const double* params, int32_t n_params,
                                         const qsg_solve_opts* opts, double* expect, qsg_stats* stats,
                                         int32_t* status, qsg_timing* timing) {
+  QSG_RANGE("qsg_mesolve_batch");
   BatchProblem P{};
   if (qsg_status s = common_setup(ctx, L, d * d, tlist, n_t, opts, P)) return s;
   if (n_points < 1) {

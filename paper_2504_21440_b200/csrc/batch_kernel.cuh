@@ -33,6 +33,12 @@ constexpr int kMaxB = 32;       // slots per batch (B = 8 CTA-local, 32 grid-wid
 constexpr int kThreads = QSG_BATCH_THREADS;  // 16 warps by default
 constexpr int W = kThreads / 32;
 constexpr int NBUF = 12;
+#ifndef QSG_BATCH_KO
+#define QSG_BATCH_KO 5  // observation pairs per reduction (2 measured no faster on TFIM-14)
+#endif
+#ifndef QSG_BATCH_KJ
+#define QSG_BATCH_KJ 15  // jump channels per reduction (5 measured no faster)
+#endif
 #ifndef QSG_BATCH_UNROLL
 #define QSG_BATCH_UNROLL 4
 #endif
@@ -651,12 +657,14 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
       int maxp = 0;
       for (int b = 0; b < B; ++b) maxp = max(maxp, S[b].phase == DONE ? 0 : S[b].n_pend);
       const int npairs = maxp * P.n_e;
-      for (int c0 = 0; c0 < npairs; c0 += 5) {  // 5 (event, e_op) pairs x 3 values per reduction
-        double oa[15];
+      // KO (event, e_op) pairs x 3 values per reduction
+      constexpr int KO = QSG_BATCH_KO;
+      for (int c0 = 0; c0 < npairs; c0 += KO) {
+        double oa[3 * KO];
 #pragma unroll
-        for (int a = 0; a < 15; ++a) oa[a] = 0.0;
+        for (int a = 0; a < 3 * KO; ++a) oa[a] = 0.0;
 #pragma unroll
-        for (int u = 0; u < 5; ++u) {
+        for (int u = 0; u < KO; ++u) {
           if (c0 + u >= npairs) continue;
           const int q = (c0 + u) / P.n_e, e = (c0 + u) % P.n_e;
           const bool act = q < S[sl].n_pend && S[sl].phase != DONE;
@@ -690,12 +698,12 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         reduce(oa);
         if (threadIdx.x < B && S[threadIdx.x].phase != DONE && out_cta) {
           Slot& s = S[threadIdx.x];
-          for (int u = 0; u < 5 && c0 + u < npairs; ++u) {
+          for (int u = 0; u < KO && c0 + u < npairs; ++u) {
             const int q = (c0 + u) / P.n_e, e = (c0 + u) % P.n_e;
             if (q >= s.n_pend) continue;
-            double2 v = make_double2(sout[threadIdx.x * 15 + 3 * u], sout[threadIdx.x * 15 + 3 * u + 1]);
+            double2 v = make_double2(sout[threadIdx.x * 3 * KO + 3 * u], sout[threadIdx.x * 3 * KO + 3 * u + 1]);
             if (P.mode == 0) {
-              const double inv = 1.0 / sout[threadIdx.x * 15 + 3 * u + 2];
+              const double inv = 1.0 / sout[threadIdx.x * 3 * KO + 3 * u + 2];
               v = make_double2(v.x * inv, v.y * inv);
             }
             P.expect[s.sys * P.n_e * P.n_t + static_cast<long long>(s.pend_grid[q]) * P.n_e + e] = v;
@@ -710,14 +718,15 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
         for (int b = 0; b < B; ++b) anyj |= (S[b].phase == JUMP);
         if (anyj) {
           const double thj = (S[sl].jump_t - S[sl].t_old) / S[sl].h_last, hl = S[sl].h_last;
-          for (int k0 = 0; k0 < P.n_c; k0 += 15) {
-            double wa[15];
+          constexpr int KJ = QSG_BATCH_KJ;  // channels per reduction (each inlines a row loop)
+          for (int k0 = 0; k0 < P.n_c; k0 += KJ) {
+            double wa[KJ];
 #pragma unroll
-            for (int u = 0; u < 15; ++u) wa[u] = 0.0;
+            for (int u = 0; u < KJ; ++u) wa[u] = 0.0;
             if (ph == JUMP) {
               rows([&](int r) {
 #pragma unroll
-                for (int u = 0; u < 15; ++u)
+                for (int u = 0; u < KJ; ++u)
                   if (k0 + u < P.n_c) {
                     const double2 v = sell_row_slot(P.c_ops[k0 + u], r,
                                                     [&](int c) { return dense_at(C, c, sl, thj, hl, SRC_DENSE); });
@@ -727,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, QSG_BATCH_MINB) batch_kernel(const _
             }
             reduce(wa);
             if (threadIdx.x < B && S[threadIdx.x].phase == JUMP)
-              for (int u = 0; u < 15 && k0 + u < P.n_c; ++u) S[threadIdx.x].w[k0 + u] = sout[threadIdx.x * 15 + u];
+              for (int u = 0; u < KJ && k0 + u < P.n_c; ++u) S[threadIdx.x].w[k0 + u] = sout[threadIdx.x * KJ + u];
           }
           __syncthreads();
           if (threadIdx.x < B && S[threadIdx.x].phase == JUMP) {

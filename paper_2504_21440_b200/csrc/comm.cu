@@ -109,6 +109,7 @@ qsg_status qsg_comm_unique_id(uint8_t* id128) {
 }
 
 qsg_status qsg_comm_init_rank(qsg_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t* id128, qsg_comm** out) {
+  QSG_RANGE("qsg_comm_init_rank");
   if (!ctx || !out || nranks < 1 || rank < 0 || rank >= nranks) {
     set_error("InvalidGrid: bad communicator arguments");
     return QSG_INVALID_GRID;
@@ -130,6 +131,7 @@ qsg_status qsg_comm_init_rank(qsg_ctx* ctx, int32_t nranks, int32_t rank, const 
 }
 
 qsg_status qsg_comm_init_all(int32_t n_dev, const int32_t* devices, qsg_comm** out) {
+  QSG_RANGE("qsg_comm_init_all");
   if (n_dev < 1 || !devices || !out) {
     set_error("InvalidGrid: bad communicator arguments");
     return QSG_INVALID_GRID;
@@ -170,6 +172,7 @@ void qsg_comm_destroy(qsg_comm* c) {
 
 // recv[r*count .. (r+1)*count) = rank r's send (doubles); host or device buffers.
 qsg_status qsg_comm_allgather(qsg_comm* c, const double* send, int64_t count, double* recv) {
+  QSG_RANGE("qsg_comm_allgather");
   if (!c || !send || !recv || count < 0) {
     set_error("InvalidGrid: bad all-gather arguments");
     return QSG_INVALID_GRID;

@@ -144,6 +144,7 @@ bool bracket(long long lo, long long hi, int nb, const long long* b, const long 
 extern "C" qsg_status qsg_ensemble_combine(int32_t n_blocks, const int64_t* block_begin,
                                            const int64_t* block_end, const double* block_sums,
                                            int64_t n_vals, int64_t n_ok_total, double* mean) {
+  QSG_RANGE("qsg_ensemble_combine");
   if (n_blocks < 1 || n_ok_total < 1) {
     set_error("EnsembleFailure: every trajectory failed");
     return QSG_ENSEMBLE_FAILURE;

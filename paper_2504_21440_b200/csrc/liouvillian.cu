@@ -339,6 +339,7 @@ extern "C" {
 
 qsg_status qsg_liouvillian_create(qsg_ctx* ctx, int64_t d, const qsg_csr* H, int32_t n_c, const qsg_csr* c_ops,
                                   qsg_op** out) {
+  QSG_RANGE("qsg_liouvillian_create");
   if (!out) {
     set_error("InvalidGrid: null output");
     return QSG_INVALID_GRID;
@@ -353,6 +354,7 @@ qsg_status qsg_liouvillian_create(qsg_ctx* ctx, int64_t d, const qsg_csr* H, int
 
 qsg_status qsg_liouvillian_export(qsg_ctx* ctx, int64_t d, const qsg_csr* H, int32_t n_c, const qsg_csr* c_ops,
                                   int64_t* nnz_out, int32_t* rowptr, int32_t* col_out, double* val_out) {
+  QSG_RANGE("qsg_liouvillian_export");
   DevBuf rp, col, val;
   long long nnz = 0;
   if (qsg_status st = assemble(ctx, d, H, n_c, c_ops, rp, col, val, nnz)) return st;

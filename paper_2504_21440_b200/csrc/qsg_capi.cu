@@ -982,6 +982,7 @@ qsg_status qsg_device_info(qsg_ctx* ctx, int* sm_count, int64_t* l2_bytes, char*
 }
 
 qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
+  QSG_RANGE("qsg_op_create");
   if (!ctx || !a || !out) {
     set_error("InvalidGrid: null argument");
     return QSG_INVALID_GRID;
@@ -1150,6 +1151,7 @@ int64_t qsg_op_rows(const qsg_op* op) { return op ? op->n_rows : 0; }
 
 qsg_status qsg_generator_apply(qsg_ctx* ctx, const qsg_generator* g, const double* params,
                                int32_t n_params, double t, const double* y, double* out) {
+  QSG_RANGE("qsg_generator_apply");
   if (!ctx || !g || g->n_terms < 1) return QSG_INVALID_GRID;
   const long long n = g->ops[0]->n_rows;
   if (qsg_status st = check_generator(g, n)) return st;
@@ -1200,6 +1202,7 @@ qsg_status qsg_mesolve(qsg_ctx* ctx, const qsg_generator* L, int64_t d, const do
                        const double* tlist, int64_t n_t, int32_t n_e, const qsg_csr* e_ops,
                        const double* params, int32_t n_params, const qsg_solve_opts* opts,
                        double* expect, double* states, qsg_stats* stats, qsg_timing* timing) {
+  QSG_RANGE("qsg_mesolve");
   if (ctx) cudaSetDevice(ctx->device);
   return run_grid_solve(ctx, 0, L, d, rho0, tlist, n_t, n_e, e_ops, params, n_params, opts, expect,
                         states, stats, timing);
@@ -1209,6 +1212,7 @@ qsg_status qsg_sesolve(qsg_ctx* ctx, const qsg_generator* G, int64_t d, const do
                        const double* tlist, int64_t n_t, int32_t n_e, const qsg_csr* e_ops,
                        const double* params, int32_t n_params, const qsg_solve_opts* opts,
                        double* expect, double* states, qsg_stats* stats, qsg_timing* timing) {
+  QSG_RANGE("qsg_sesolve");
   if (ctx) cudaSetDevice(ctx->device);
   return run_grid_solve(ctx, 1, G, d, psi0, tlist, n_t, n_e, e_ops, params, n_params, opts, expect,
                         states, stats, timing);

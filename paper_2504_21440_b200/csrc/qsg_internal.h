@@ -3,6 +3,7 @@
 
 #include <atomic>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <string>
 #include <vector>
@@ -103,3 +104,13 @@ qsg_status build_events(const double* tlist, long long n_t, const qsg_solve_opts
 qsg_status status_from_device(int st, double t);
 
 }  // namespace qsg
+
+// NVTX range over a C-ABI entry point (named in nsys timelines and `ncu --nvtx` filters); NVTX v3 is
+// header-only and costs nothing unless a tool is attached.
+struct QsgRange {
+  explicit QsgRange(const char* name) { nvtxRangePushA(name); }
+  ~QsgRange() { nvtxRangePop(); }
+  QsgRange(const QsgRange&) = delete;
+  QsgRange& operator=(const QsgRange&) = delete;
+};
+#define QSG_RANGE(name) QsgRange qsg_nvtx_range_(name)

@@ -579,6 +579,7 @@ qsg_status qsg_ssesolve(qsg_ctx* ctx, const qsg_generator* G, int64_t d, int32_t
                         const double* params, int32_t n_params, uint64_t seed, int64_t traj_begin,
                         int64_t traj_end, double dt_max, int32_t store_measurement, qsg_sde_out* out,
                         qsg_timing* timing) {
+  QSG_RANGE("qsg_ssesolve");
   return run_sde(ctx, 0, G, d, n_sc, sc_ops, n_e, e_ops, psi0, tlist, n_t, params, n_params, seed, traj_begin,
                  traj_end, dt_max, store_measurement, out, timing);
 }
@@ -588,6 +589,7 @@ qsg_status qsg_smesolve(qsg_ctx* ctx, const qsg_generator* L, int64_t d, int32_t
                         const double* params, int32_t n_params, uint64_t seed, int64_t traj_begin,
                         int64_t traj_end, double dt_max, int32_t store_measurement, qsg_sde_out* out,
                         qsg_timing* timing) {
+  QSG_RANGE("qsg_smesolve");
   return run_sde(ctx, 1, L, d, n_sc, sc_ops, n_e, e_ops, rho0, tlist, n_t, params, n_params, seed, traj_begin,
                  traj_end, dt_max, store_measurement, out, timing);
 }

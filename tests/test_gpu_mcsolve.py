@@ -56,6 +56,26 @@ def test_mc_decay_law_and_oracle_parity(ctx):
     _compare_trajectories(dev, ref)
 
 
+def test_mc_disjoint_seeds_ks(ctx):
+    """test_trajectories.cpp:186-203 on the device: first-jump times of 400 decaying-qubit
+    trajectories from seeds 1000 and 2000 pass a two-sample KS test (p > 0.01, scipy's ks_2samp
+    for the reference's test::ks_two_sample_pvalue), and each sample passes a one-sample KS test
+    against the exact first-jump law 1 - exp(-gamma t), truncated at t = 40."""
+    from scipy.stats import ks_2samp, kstest
+    m = O.Model("decay2", 0.5)
+    t = np.linspace(0.0, 40.0, 21)
+    samples = []
+    for seed in (1000, 2000):
+        r = _mc(ctx, m, t, seed, 0, 400)
+        assert r["n_ok"] == 400
+        samples.append(np.array([j[0][0] for j in r["jumps"] if len(j)]))
+        ref = m.mcsolve(t, seed, 32)  # the same draws as the restatement, trajectory by trajectory
+        _compare_trajectories(r, ref)
+    assert ks_2samp(samples[0], samples[1]).pvalue > 0.01
+    for x in samples:
+        assert kstest(x, lambda v: (1.0 - np.exp(-0.5 * v)) / (1.0 - np.exp(-20.0))).pvalue > 0.01
+
+
 def test_mc_jc_per_trajectory_parity(ctx):
     m = O.Model("jc", 6, 1.0, 1.0, 0.1, 0.05, 0.05)
     t = np.linspace(0, 60, 61)
