@@ -349,29 +349,37 @@ __global__ void sell_code_fill_dense_kernel(const int* rowptr, const unsigned* s
   for (int k = 0; k < e - b; ++k) scode[base + (k >> 3) * 256 + (k & 7)] = static_cast<T>(dense[slot_of[b + k]]);
 }
 
-// Aligned code fill: one warp per 32-row slice. Within each row the entries are reordered by
-// (how many rows of the slice hold an entry at the same distance |col - row| (descending), that
-// distance, the signed offset), so the rows of a slice put their common entries at the same SELL
-// position. A warp's lookups at one position then touch one or two dictionary words (a broadcast or
-// a +/- offset pair) instead of up to 32, and its gathers hit one contiguous segment. TFIM-10
-// Liouvillian: 4.70 -> 1.71 distinct codes per (slice, position), 34% -> 93% with at most two
-// (scripts/coded_align_stats.py). The row's sum runs in the new order. Slices whose rows exceed
-// kAlignMaxRow entries or whose distance set overflows the per-warp table keep the CSR order.
+// Slice-aligned entry order (coded and plain SELL fills): one warp per 32-row slice. Within each
+// row the entries are reordered by (how many rows of the slice hold an entry at the same distance
+// |col - row| (descending), that distance, the signed offset), so the rows of a slice put their
+// common entries at the same SELL position. A warp's dictionary lookups at one position then touch
+// one or two words (a broadcast or a +/- offset pair) instead of up to 32, and its gathers hit one
+// contiguous segment. TFIM-10 Liouvillian: 4.70 -> 1.71 distinct codes per (slice, position), 34% ->
+// 93% with at most two (scripts/coded_align_stats.py). The row's sum runs in the new order. Slices
+// whose rows exceed kAlignMaxRow entries or whose distance set overflows the per-warp table keep
+// the CSR order. QSG_SELL_ALIGN=0 keeps the CSR order in the coded store too.
 constexpr int kAlignMaxRow = 64;
 constexpr int kAlignTab = 256;  // distinct distances per slice (open addressing, per warp)
 constexpr int kAlignWarps = 4;
 
-template <class T>
-__global__ void __launch_bounds__(32 * kAlignWarps) sell_code_fill_aligned_kernel(
-    const int* __restrict__ rowptr, const int* __restrict__ col, const unsigned* __restrict__ slot_of,
-    const unsigned* __restrict__ dense, int n, const long long* __restrict__ code_off, T* scode) {
-  __shared__ int s_key[kAlignWarps][kAlignTab];
-  __shared__ int s_cnt[kAlignWarps][kAlignTab];
-  __shared__ int s_bad[kAlignWarps];
+bool sell_align_enabled() {
+  const char* al = std::getenv("QSG_SELL_ALIGN");
+  return !(al && al[0] == '0');
+}
+// The plain store keeps the CSR (reference) order unless QSG_PLAIN_ALIGN=1: aligned plain rows
+// measured sweep 98.5 -> 95.3 ms, TFIM-14 mcsolve unchanged, K-cluster Kerr-50 9.47 -> 9.54 us per
+// attempt (profiles/r02_sell_align.log), not enough to give up the reference summation order.
+bool plain_align_enabled() {
+  const char* al = std::getenv("QSG_PLAIN_ALIGN");
+  return al && al[0] == '1' && sell_align_enabled();
+}
+
+// Fills pm[0..len) with the lane's row order (indices into the row's CSR entries); false: keep
+// the CSR order for this slice. Every lane of the warp must call it.
+__device__ bool slice_aligned_order(const int* __restrict__ col, int r, int b, int len, bool live,
+                                    int (*s_key)[kAlignTab], int (*s_cnt)[kAlignTab], int* s_bad,
+                                    unsigned char* pm) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long r = (static_cast<long long>(blockIdx.x) * kAlignWarps + w) * 32 + lane;
-  const bool live = r < n;
-  const int b = live ? rowptr[r] : 0, len = live ? rowptr[r + 1] - b : 0;
   for (int i = lane; i < kAlignTab; i += 32) {
     s_key[w][i] = -1;
     s_cnt[w][i] = 0;
@@ -393,26 +401,17 @@ __global__ void __launch_bounds__(32 * kAlignWarps) sell_code_fill_aligned_kerne
   __syncwarp();
   if (!s_bad[w])
     for (int k = 0; k < len; ++k) {
-      const int a = abs(col[b + k] - static_cast<int>(r));
-      const int h = slot_of_dist(a, true);
+      const int h = slot_of_dist(abs(col[b + k] - r), true);
       if (h < 0) s_bad[w] = 1;
       else atomicAdd(&s_cnt[w][h], 1);
     }
   __syncwarp();
-  if (!live) return;
-  const long long base = code_off[r >> 5] + (r & 31) * 8;
-  if (s_bad[w]) {  // CSR order
-    for (int k = 0; k < len; ++k) scode[base + (k >> 3) * 256 + (k & 7)] = static_cast<T>(dense[slot_of[b + k]]);
-    return;
-  }
-  // per entry: frequency, distance, signed offset; insertion sort of the positions
+  if (!live || s_bad[w]) return false;
   int fq[kAlignMaxRow], ds[kAlignMaxRow], of[kAlignMaxRow];
-  unsigned char pm[kAlignMaxRow];
   for (int k = 0; k < len; ++k) {
-    const int o = col[b + k] - static_cast<int>(r);
-    const int a = abs(o);
-    fq[k] = s_cnt[w][slot_of_dist(a, false)];
-    ds[k] = a;
+    const int o = col[b + k] - r;
+    ds[k] = abs(o);
+    fq[k] = s_cnt[w][slot_of_dist(ds[k], false)];
     of[k] = o;
     pm[k] = static_cast<unsigned char>(k);
   }
@@ -421,7 +420,7 @@ __global__ void __launch_bounds__(32 * kAlignWarps) sell_code_fill_aligned_kerne
     if (ds[x] != ds[y]) return ds[x] < ds[y];
     return of[x] < of[y];
   };
-  for (int i = 1; i < len; ++i) {
+  for (int i = 1; i < len; ++i) {  // insertion sort (stable)
     const unsigned char v = pm[i];
     int j = i - 1;
     while (j >= 0 && before(v, pm[j])) {
@@ -430,8 +429,45 @@ __global__ void __launch_bounds__(32 * kAlignWarps) sell_code_fill_aligned_kerne
     }
     pm[j + 1] = v;
   }
+  return true;
+}
+
+template <class T>
+__global__ void __launch_bounds__(32 * kAlignWarps) sell_code_fill_aligned_kernel(
+    const int* __restrict__ rowptr, const int* __restrict__ col, const unsigned* __restrict__ slot_of,
+    const unsigned* __restrict__ dense, int n, const long long* __restrict__ code_off, T* scode) {
+  __shared__ int s_key[kAlignWarps][kAlignTab];
+  __shared__ int s_cnt[kAlignWarps][kAlignTab];
+  __shared__ int s_bad[kAlignWarps];
+  const long long r = (static_cast<long long>(blockIdx.x) * kAlignWarps + (threadIdx.x >> 5)) * 32 + (threadIdx.x & 31);
+  const bool live = r < n;
+  const int b = live ? rowptr[r] : 0, len = live ? rowptr[r + 1] - b : 0;
+  unsigned char pm[kAlignMaxRow];
+  const bool sorted = slice_aligned_order(col, static_cast<int>(r), b, len, live, s_key, s_cnt, s_bad, pm);
+  if (!live) return;
+  const long long base = code_off[r >> 5] + (r & 31) * 8;
   for (int k = 0; k < len; ++k)
-    scode[base + (k >> 3) * 256 + (k & 7)] = static_cast<T>(dense[slot_of[b + pm[k]]]);
+    scode[base + (k >> 3) * 256 + (k & 7)] = static_cast<T>(dense[slot_of[b + (sorted ? pm[k] : k)]]);
+}
+
+__global__ void __launch_bounds__(32 * kAlignWarps) sell_fill_aligned_kernel(
+    const int* __restrict__ rowptr, const int* __restrict__ col, const double2* __restrict__ val, int n,
+    const long long* __restrict__ slice_off, int* scol, double2* sval) {
+  __shared__ int s_key[kAlignWarps][kAlignTab];
+  __shared__ int s_cnt[kAlignWarps][kAlignTab];
+  __shared__ int s_bad[kAlignWarps];
+  const long long r = (static_cast<long long>(blockIdx.x) * kAlignWarps + (threadIdx.x >> 5)) * 32 + (threadIdx.x & 31);
+  const bool live = r < n;
+  const int b = live ? rowptr[r] : 0, len = live ? rowptr[r + 1] - b : 0;
+  unsigned char pm[kAlignMaxRow];
+  const bool sorted = slice_aligned_order(col, static_cast<int>(r), b, len, live, s_key, s_cnt, s_bad, pm);
+  if (!live) return;
+  const long long base = slice_off[r >> 5] * 32 + (r & 31);
+  for (int k = 0; k < len; ++k) {
+    const int e = b + (sorted ? pm[k] : k);
+    scol[base + 32LL * k] = col[e];
+    sval[base + 32LL * k] = val[e];
+  }
 }
 
 // Builds the coded store of `op` from the staged CSR; leaves op plain when the operator has more
@@ -476,8 +512,7 @@ static cudaError_t build_coded_store(qsg_op* op, const int* rp, const int* col, 
   cudaMemcpyAsync(op->code_off, coff.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(op->dict_off, doff.p, sizeof(int) * count, cudaMemcpyDeviceToDevice, s);
   cudaMemcpyAsync(op->dict_val, dval.p, sizeof(double2) * count, cudaMemcpyDeviceToDevice, s);
-  const char* al = std::getenv("QSG_CODED_ALIGN");
-  const bool align = !(al && al[0] == '0');
+  const bool align = sell_align_enabled();
   const unsigned nba = static_cast<unsigned>((nsl + kAlignWarps - 1) / kAlignWarps);
   if (cbytes == 1) {
     if (align)
@@ -1187,8 +1222,13 @@ qsg_status qsg_op_create(qsg_ctx* ctx, const qsg_csr* a, qsg_op** out) {
     cudaMemsetAsync(op->col, 0, sizeof(int) * pe, s);
     cudaMemsetAsync(op->val, 0, sizeof(double2) * pe, s);
     mark("memset");
-    sell_fill_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-        srp, scol, sval, static_cast<int>(n), op->slice_off, op->col, op->val);
+    if (plain_align_enabled())
+      sell_fill_aligned_kernel<<<static_cast<unsigned>(((n + 31) / 32 + kAlignWarps - 1) / kAlignWarps),
+                                 32 * kAlignWarps, 0, s>>>(srp, scol, sval, static_cast<int>(n), op->slice_off,
+                                                           op->col, op->val);
+    else
+      sell_fill_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+          srp, scol, sval, static_cast<int>(n), op->slice_off, op->col, op->val);
     if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(s))) {
       qsg_op_destroy(op);
       return cuda_fail(e, "operator store build");
