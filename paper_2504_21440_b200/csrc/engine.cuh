@@ -180,9 +180,12 @@ __device__ __forceinline__ CodedView coded_view(const DevSell& A) {
 }
 
 // Coded row with the dictionary staged in shared memory (sval / soff point into __shared__).
-template <class XF>
+// CB: code bytes fixed at compile time (1 or 2; 0 reads A.cbytes), so the unrolled loop carries
+// no per-entry code-width test
+template <int CB = 0, class XF>
 __device__ __forceinline__ double2 sell_row_coded_smem(const CodedView& A, const double2* sval, const int* soff,
                                                        int row, int len, long long base, XF&& xf) {
+  const int cbytes = CB ? CB : A.cbytes;
   __builtin_assume(__isShared(sval));
   __builtin_assume(__isShared(soff));
   double2 acc = make_double2(0.0, 0.0);
@@ -192,7 +195,7 @@ __device__ __forceinline__ double2 sell_row_coded_smem(const CodedView& A, const
     for (int c = 0; c < 4; ++c) {
       const int j = j0 + 8 * c;
       if (j < len) {
-        if (A.cbytes == 1) {
+        if (cbytes == 1) {
           const uint2 v = ld_stream_u2(reinterpret_cast<const uint2*>(A.code8 + base + 32LL * j));
           w[c] = make_uint4(v.x, v.y, 0u, 0u);
         } else {
@@ -209,7 +212,7 @@ __device__ __forceinline__ double2 sell_row_coded_smem(const CodedView& A, const
         const int j = j0 + 8 * c + u;
         if (j < len) {
           unsigned k;
-          if (A.cbytes == 1) k = ((u < 4 ? w[c].x : w[c].y) >> (8 * (u & 3))) & 0xffu;
+          if (cbytes == 1) k = ((u < 4 ? w[c].x : w[c].y) >> (8 * (u & 3))) & 0xffu;
           else k = ((u < 2 ? w[c].x : u < 4 ? w[c].y : u < 6 ? w[c].z : w[c].w) >> (16 * (u & 1))) & 0xffffu;
           cfma(sval[k], xf(row + soff[k]), acc);
         }

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
+#include <type_traits>
 
 #include "engine.cuh"
 #include "grid_engine.h"
@@ -453,46 +454,52 @@ __device__ __forceinline__ double stage_pass(const GridProblem& P, const Ctl& c,
         len = __ldg(rowlen + b * 32 + lane);
         base = __ldg(code_off + b) + 8LL * lane;  // interleaved groups of 8 codes
       };
-      int b = s0 + warp, len = 0;
-      long long base = 0;
-      if (b < s1) meta(b, len, base);
-      for (; b < s1; b += W) {
-        const int bn = b + W;
-        int len_n = 0;
-        long long base_n = 0;
-        if (bn < s1) meta(bn, len_n, base_n);
-        const int row = (b << 5) + lane;
-        const bool ok = row < n;
-        Ops o;
-        const double2 k = sval ? sell_row_coded_smem(cv, sval, soff, row, len, base, xin)
-                               : sell_row_coded_v(cv, row, len, base, xin);
-        if (bn < s1) {
-          // the next slice's code block (32 rows x width codes, contiguous): one sector run per lane
-          const long long cb_n = base_n - 8LL * lane;
-          const char* blk = cv.cbytes == 1 ? reinterpret_cast<const char*>(cv.code8 + cb_n)
-                                           : reinterpret_cast<const char*>(cv.code16 + cb_n);
-          prefetch_l2(blk + lane * 32 * cv.cbytes);  // 1 KB x code bytes window (array padded by 1 K codes)
-          const int rn = (bn << 5) + lane;
-          if (rn < n) {
-            prefetch_l2(y + rn);
-            prefetch_l2(k1 + rn);
-            if (S >= 3 && S <= 5) prefetch_l2(pk2 + rn);
-            if (S >= 4) prefetch_l2(pk3 + rn);
-            if (S >= 5) prefetch_l2(pk4 + rn);
-            if (S >= 6) prefetch_l2(pk5 + rn);
-            if (S == 7) {
-              prefetch_l2(pk6 + rn);
-              prefetch_l2(x + rn);
+      // the slice loop instantiated per code width (one copy runs): no per-entry width test
+      auto slices = [&](auto cb) {
+        constexpr int CB = decltype(cb)::value;
+        int b = s0 + warp, len = 0;
+        long long base = 0;
+        if (b < s1) meta(b, len, base);
+        for (; b < s1; b += W) {
+          const int bn = b + W;
+          int len_n = 0;
+          long long base_n = 0;
+          if (bn < s1) meta(bn, len_n, base_n);
+          const int row = (b << 5) + lane;
+          const bool ok = row < n;
+          Ops o;
+          const double2 k = sval ? sell_row_coded_smem<CB>(cv, sval, soff, row, len, base, xin)
+                                 : sell_row_coded_v(cv, row, len, base, xin);
+          if (bn < s1) {
+            // the next slice's code block (32 rows x width codes, contiguous): one sector run per lane
+            const long long cb_n = base_n - 8LL * lane;
+            const char* blk = cv.cbytes == 1 ? reinterpret_cast<const char*>(cv.code8 + cb_n)
+                                             : reinterpret_cast<const char*>(cv.code16 + cb_n);
+            prefetch_l2(blk + lane * 32 * cv.cbytes);  // 1 KB x code bytes window (array padded by 1 K codes)
+            const int rn = (bn << 5) + lane;
+            if (rn < n) {
+              prefetch_l2(y + rn);
+              prefetch_l2(k1 + rn);
+              if (S >= 3 && S <= 5) prefetch_l2(pk2 + rn);
+              if (S >= 4) prefetch_l2(pk3 + rn);
+              if (S >= 5) prefetch_l2(pk4 + rn);
+              if (S >= 6) prefetch_l2(pk5 + rn);
+              if (S == 7) {
+                prefetch_l2(pk6 + rn);
+                prefetch_l2(x + rn);
+              }
             }
           }
+          // operands after the SpMV: they were prefetched into L2 one slice ahead, and holding them in
+          // registers across the SpMV only spills (measured 30.8 ms vs 33.8 ms per TFIM-10 solve)
+          load_operands(row, ok, o);
+          if (ok) epilogue(row, k, o);
+          len = len_n;
+          base = base_n;
         }
-        // operands after the SpMV: they were prefetched into L2 one slice ahead, and holding them in
-        // registers across the SpMV only spills (measured 30.8 ms vs 33.8 ms per TFIM-10 solve)
-        load_operands(row, ok, o);
-        if (ok) epilogue(row, k, o);
-        len = len_n;
-        base = base_n;
-      }
+      };
+      if (cv.cbytes == 1) slices(std::integral_constant<int, 1>{});
+      else slices(std::integral_constant<int, 2>{});
       return esq;
     }
   }
