@@ -206,17 +206,20 @@ __device__ __forceinline__ double2 sell_row_coded_smem(const CodedView& A, const
       }
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int c = 0; c < 4; ++c) {
+      // entries of this group present in the row, compared with the unrolled index (one ISETP per
+      // entry, no per-entry add: TFIM-10 solve 23.08 -> 22.51 ms)
+      const int rem = len - (j0 + 8 * c);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int j = j0 + 8 * c + u;
-        if (j < len) {
+        if (u < rem) {
           unsigned k;
           if (cbytes == 1) k = ((u < 4 ? w[c].x : w[c].y) >> (8 * (u & 3))) & 0xffu;
           else k = ((u < 2 ? w[c].x : u < 4 ? w[c].y : u < 6 ? w[c].z : w[c].w) >> (16 * (u & 1))) & 0xffffu;
           cfma(sval[k], xf(row + soff[k]), acc);
         }
       }
+    }
   }
   return acc;
 }
