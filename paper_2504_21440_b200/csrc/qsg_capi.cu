@@ -190,11 +190,43 @@ __global__ void __launch_bounds__(256) gen_apply_kernel(DevGen g, const double* 
   }
 }
 
+// Single-term coded generator: the dictionary staged in shared memory and the slice loop
+// instantiated per code width, as in the grid engine's stage passes (K-spmv).
+template <int CB>
+__global__ void __launch_bounds__(256) gen_apply_coded_kernel(const DevSell A, int n, const double2* __restrict__ y,
+                                                              double2* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  double2* sv = reinterpret_cast<double2*>(s_dyn);
+  int* so = reinterpret_cast<int*>(sv + A.dict_n);
+  for (int i = threadIdx.x; i < A.dict_n; i += blockDim.x) {
+    sv[i] = A.dict_val[i];
+    so[i] = A.dict_off[i];
+  }
+  __syncthreads();
+  const CodedView cv = coded_view(A);
+  const int W = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int nsl = (n + 31) >> 5;
+  for (int sl = blockIdx.x * W + (threadIdx.x >> 5); sl < nsl; sl += gridDim.x * W) {
+    const int row = (sl << 5) + lane;
+    const int len = __ldg(A.rowlen + row);
+    const long long base = __ldg(A.code_off + sl) + 8LL * lane;
+    const double2 k = sell_row_coded_smem<CB>(cv, sv, so, row, len, base, [&](int c) { return y[c]; });
+    if (row < n) out[row] = k;
+  }
+}
+
 static cudaError_t launch_apply(const DevGen& dg, const double* params, int n, double t,
                                 const double2* y, double2* out, int sms, cudaStream_t s) {
   const int threads = 256;
   const int nsl = (n + 31) / 32;
   const int grid = std::max(1, std::min((nsl + 7) / 8, sms * 8));
+  const DevSell& A = dg.A[0];
+  if (dg.n_terms == 1 && A.code_bytes > 0 && A.dict_n > 0 && A.dict_n <= 2048) {
+    const size_t smem = static_cast<size_t>(A.dict_n) * (sizeof(double2) + sizeof(int));
+    if (A.code_bytes == 1) gen_apply_coded_kernel<1><<<grid, threads, smem, s>>>(A, n, y, out);
+    else gen_apply_coded_kernel<2><<<grid, threads, smem, s>>>(A, n, y, out);
+    return cudaGetLastError();
+  }
   gen_apply_kernel<<<grid, threads, 0, s>>>(dg, params, n, t, y, out);
   return cudaGetLastError();
 }

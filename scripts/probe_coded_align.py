@@ -1,5 +1,5 @@
 """Dev probe: TFIM-10 mesolve (configs[1]) and the TFIM-10 coded SpMV with the coded store's
-entries in CSR order (QSG_CODED_ALIGN=0) vs slice-aligned order (default), same process."""
+entries in CSR order (QSG_SELL_ALIGN=0) vs slice-aligned order (default), same process."""
 import json, os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -10,7 +10,7 @@ m = q.Model("ising", 10, 1, 1.0, 0.2, 1.0, 1)
 L = m.export(q.SEL_L_CONST)
 gens = {}
 for mode in ("0", "1"):
-    os.environ["QSG_CODED_ALIGN"] = mode
+    os.environ["QSG_SELL_ALIGN"] = mode
     gens[mode] = q.Generator([ctx.op(L)])
 eops = [m.export(q.SEL_E_OP, k) for k in range(m.n_eops)]
 psi = m.psi0()
