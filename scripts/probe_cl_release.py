@@ -1,5 +1,7 @@
 """Dev probe: K-cluster barrier with a shared-memory-only release (default) vs the full
-arrive.release (QSG_CL_FULL_RELEASE=1), interleaved, Kerr mesolve; per-attempt time and agreement."""
+arrive.release (QSG_CL_FULL_RELEASE=1), interleaved, Kerr mesolve; per-attempt time and agreement.
+The switch existed only for this A/B (profiles/r02_cl_release.log) and was removed once the
+shared-memory release became the only form: today both modes run the same kernel."""
 import json, os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
