@@ -183,6 +183,51 @@ __device__ __forceinline__ void sync_all(const GridProblem& P, int G) {
   }
 }
 
+// sesolve observations <psi|E psi> (evolve.cpp:341-345) with psi(theta) materialised once per
+// event in SB (free from the end of stage 2, or of stage 6 for a flush, until stage 3 writes it):
+// each e_op entry then gathers one amplitude instead of evaluating the 8-vector dense output, and
+// the e_ops share one evaluation. TFIM-20 (3 e_ops of 20 entries per row, 100 events): the
+// observations were 41% of the solve. Same values and summation order as observe_pass. Every CTA
+// calls it (grid barriers inside); sb_busy: SB is still being gathered (materialised stage-2 input).
+__device__ __noinline__ void observe_se(const GridProblem& P, const Ctl& c, double* slots, double* smem, int rank,
+                                        int G, bool sb_busy) {
+  double2* const* p = c.p;
+  const int np = c.np;
+  const double h_last = c.h_last;
+  const int gtid = rank * blockDim.x + threadIdx.x;
+  const int gstride = G * blockDim.x;
+  double2* psi = p[SB];
+  for (int q = 0; q < np; ++q) {
+    if (q > 0 || sb_busy) sync_all(P, G);  // nobody still gathers SB
+    const double th = c.pend[q].theta;
+    for (int r = gtid; r < P.n; r += gstride) psi[r] = dense_at(p, r, th, h_last);
+    sync_all(P, G);
+    for (int e = 0; e < P.n_e; ++e) {
+      double2 acc = make_double2(0.0, 0.0);
+      if (c.pend[q].grid_idx >= 0) {
+        const int* rp = P.se_rowptr + static_cast<long long>(e) * (P.n + 1);
+        const long long off = P.se_off[e];
+        for (int r = gtid; r < P.n; r += gstride) {
+          double2 ev = make_double2(0.0, 0.0);
+          for (int k = rp[r]; k < rp[r + 1]; ++k) ev = cadd(ev, cmul(P.se_val[off + k], psi[P.se_col[off + k]]));
+          acc = cadd(acc, cmul(cconj(psi[r]), ev));
+        }
+      }
+      const double sx = block_sum(acc.x, smem);
+      const double sy = block_sum(acc.y, smem);
+      if (threadIdx.x == 0) {
+        const int s = 2 * (q * P.n_e + e);
+        slots[static_cast<long long>(s) * G + rank] = sx;
+        slots[static_cast<long long>(s + 1) * G + rank] = sy;
+      }
+    }
+    if (c.pend[q].save_idx >= 0) {  // state save: every CTA writes its share
+      double2* out = P.states + static_cast<long long>(c.pend[q].save_idx) * P.n;
+      for (int r = gtid; r < P.n; r += gstride) out[r] = psi[r];
+    }
+  }
+}
+
 __device__ __forceinline__ void push_pending(const GridProblem& P, Ctl& c, double theta) {
   c.pend[c.np] = Pending{theta, c.ev_grid[c.next], c.ev_save[c.next]};
   ++c.np;
@@ -667,7 +712,8 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
   auto slots = [&](int par) { return red + static_cast<long long>(kSlotObs0 + par * kObsSlots) * G; };
   // observation flush: pass, barrier, CTA-0 commit (double-buffered slots)
   auto flush_obs = [&]() {
-    observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
+    if (MODE == 1) observe_se(P, c, slots(c.obs_par), s_red, rank, G, false);
+    else observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
     sync_all(P, G);
     observe_commit(P, c, slots(c.obs_par), G);
     __syncthreads();
@@ -814,7 +860,10 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
     } else {
       stage_pass<2, ST == 2 ? 1 : ST>(P, c, s0, s1, sval, soff, &ring);
     }
-    if (c.np) observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
+    if (c.np) {
+      if (MODE == 1) observe_se(P, c, slots(c.obs_par), s_red, rank, G, PF && P.x2 && !P.k1g);
+      else observe_pass<MODE>(P, c, slots(c.obs_par), s_red, rank, G);
+    }
     sync_all(P, G);
     if (c.np) {
       observe_commit(P, c, slots(c.obs_par), G);
