@@ -104,6 +104,12 @@ __device__ __noinline__ void observe_pass(const GridProblem& P, const Ctl& c, do
             const double2 rh = cscale(0.5, cadd(rji, cconj(rij)));
             acc = cadd(acc, cmul(P.eo_v[k], rh));
           }
+        } else if (P.n_se_ops == P.n_e) {  // e_op operator stores (observe_se)
+          for (int r = gtid; r < P.n; r += gstride) {
+            const double2 ev =
+                sell_row(P.se_ops[e], r >> 5, r & 31, [&](int col) { return dense_at(p, col, th, h_last); });
+            acc = cadd(acc, cmul(cconj(dense_at(p, r, th, h_last)), ev));
+          }
         } else {
           const int* rp = P.se_rowptr + static_cast<long long>(e) * (P.n + 1);
           const long long off = P.se_off[e];
@@ -205,12 +211,21 @@ __device__ __noinline__ void observe_se(const GridProblem& P, const Ctl& c, doub
     for (int e = 0; e < P.n_e; ++e) {
       double2 acc = make_double2(0.0, 0.0);
       if (c.pend[q].grid_idx >= 0) {
-        const int* rp = P.se_rowptr + static_cast<long long>(e) * (P.n + 1);
-        const long long off = P.se_off[e];
-        for (int r = gtid; r < P.n; r += gstride) {
-          double2 ev = make_double2(0.0, 0.0);
-          for (int k = rp[r]; k < rp[r + 1]; ++k) ev = cadd(ev, cmul(P.se_val[off + k], psi[P.se_col[off + k]]));
-          acc = cadd(acc, cmul(cconj(psi[r]), ev));
+        if (P.n_se_ops == P.n_e) {
+          // the e_op's operator store: a warp's rows are one SELL slice (gtid = lane mod 32)
+          const DevSell& E = P.se_ops[e];
+          for (int r = gtid; r < P.n; r += gstride) {
+            const double2 ev = sell_row(E, r >> 5, r & 31, [&](int col) { return psi[col]; });
+            acc = cadd(acc, cmul(cconj(psi[r]), ev));
+          }
+        } else {
+          const int* rp = P.se_rowptr + static_cast<long long>(e) * (P.n + 1);
+          const long long off = P.se_off[e];
+          for (int r = gtid; r < P.n; r += gstride) {
+            double2 ev = make_double2(0.0, 0.0);
+            for (int k = rp[r]; k < rp[r + 1]; ++k) ev = cadd(ev, cmul(P.se_val[off + k], psi[P.se_col[off + k]]));
+            acc = cadd(acc, cmul(cconj(psi[r]), ev));
+          }
         }
       }
       const double sx = block_sum(acc.x, smem);
@@ -1264,13 +1279,21 @@ __global__ void __launch_bounds__(kClThreads, 1) dp5_cluster_kernel(const __grid
           const int q = pr / P.n_e, e = pr % P.n_e;
           const double th = c.pend[q].theta;
           if (c.pend[q].grid_idx < 0) continue;
-          const int* rp = P.se_rowptr + static_cast<long long>(e) * (P.n + 1);
-          const long long off = P.se_off[e];
-          for (int r = r0 + tid; r < r1; r += nthr) {
-            double2 ev = make_double2(0.0, 0.0);
-            for (int k = rp[r]; k < rp[r + 1]; ++k)
-              ev = cadd(ev, cmul(P.se_val[off + k], cl_dense(p, P.se_col[off + k], th, hl, R, L.rmagic)));
-            acc[v] = cadd(acc[v], cmul(cconj(cl_dense(p, r, th, hl, R, L.rmagic)), ev));
+          if (P.n_se_ops == P.n_e) {  // e_op operator stores (r0 and the strides are multiples of 32)
+            for (int r = r0 + tid; r < r1; r += nthr) {
+              const double2 ev = sell_row(P.se_ops[e], r >> 5, r & 31,
+                                          [&](int col) { return cl_dense(p, col, th, hl, R, L.rmagic); });
+              acc[v] = cadd(acc[v], cmul(cconj(cl_dense(p, r, th, hl, R, L.rmagic)), ev));
+            }
+          } else {
+            const int* rp = P.se_rowptr + static_cast<long long>(e) * (P.n + 1);
+            const long long off = P.se_off[e];
+            for (int r = r0 + tid; r < r1; r += nthr) {
+              double2 ev = make_double2(0.0, 0.0);
+              for (int k = rp[r]; k < rp[r + 1]; ++k)
+                ev = cadd(ev, cmul(P.se_val[off + k], cl_dense(p, P.se_col[off + k], th, hl, R, L.rmagic)));
+              acc[v] = cadd(acc[v], cmul(cconj(cl_dense(p, r, th, hl, R, L.rmagic)), ev));
+            }
           }
         }
       }

@@ -19,6 +19,8 @@ struct GridCtl {
   int final_buf;
 };
 
+constexpr int kGridMaxSeOps = 8;  // sesolve e_ops kept as operator stores
+
 struct GridProblem {
   int cluster;    // 1: the whole grid is one thread-block cluster (hardware cluster barriers)
   int smem_dict;  // > 0: the single-term coded generator's dictionary (entries) staged in shared memory
@@ -47,6 +49,10 @@ struct GridProblem {
   const int* se_col;
   const double2* se_val;
   const long long* se_off;
+  // sesolve observation through operator stores (plain or dictionary-coded, like the generator's)
+  // instead of the CSR above when n_se_ops == n_e
+  int n_se_ops;
+  DevSell se_ops[kGridMaxSeOps];
   double2* expect;  // n_e x n_grid, column-major
   double2* states;  // n_save x n
   GridCtl* ctl;

@@ -898,6 +898,8 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   std::vector<double> eo_v;
   std::vector<long long> se_off;
   std::vector<int> se_col;
+  const char* es = std::getenv("QSG_SE_EOP_STORE");
+  const bool se_store = mode == 1 && n_e > 0 && n_e <= kGridMaxSeOps && !(es && es[0] == '0');
   for (int e = 0; e < n_e; ++e) {
     const qsg_csr& A = e_ops[e];
     if (mode == 0) {
@@ -909,12 +911,30 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
           eo_v.push_back(A.val[2 * p + 1]);
         }
       eo_off.push_back(static_cast<int>(eo_i.size()));
-    } else {
+    } else if (!se_store) {
       se_off.push_back(static_cast<long long>(se_col.size()));
       se_rowptr.insert(se_rowptr.end(), A.rowptr, A.rowptr + A.n_rows + 1);
       se_col.insert(se_col.end(), A.col, A.col + A.nnz);
       eo_v.insert(eo_v.end(), A.val, A.val + 2 * A.nnz);
     }
+  }
+  // sesolve: e_ops as operator stores (the coded store shrinks e.g. a 20-spin Sx total from 420 MB
+  // to ~25 MB per evaluation); QSG_SE_EOP_STORE=0 keeps the CSR path
+  struct OpHold {
+    std::vector<qsg_op*> v;
+    ~OpHold() {
+      for (qsg_op* o : v) qsg_op_destroy(o);
+    }
+  } se_hold;
+  P.n_se_ops = 0;
+  if (se_store) {
+    for (int e = 0; e < n_e; ++e) {
+      qsg_op* o = nullptr;
+      if (qsg_status st = qsg_op_create(ctx, &e_ops[e], &o)) return st;
+      se_hold.v.push_back(o);
+      P.se_ops[e] = sell_view(o, true);
+    }
+    P.n_se_ops = n_e;
   }
   DevBuf d_eoff, d_ei, d_ej, d_ev, d_srp, d_scol, d_soff;
   if (mode == 0) {
@@ -927,7 +947,7 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
     P.eo_i = d_ei.as<int>();
     P.eo_j = d_ej.as<int>();
     P.eo_v = d_ev.as<double2>();
-  } else {
+  } else if (P.n_se_ops == 0) {
     if ((ce = upload(d_srp, se_rowptr.data(), se_rowptr.size() * sizeof(int), s)) ||
         (ce = upload(d_scol, se_col.data(), se_col.size() * sizeof(int), s)) ||
         (ce = upload(d_ev, eo_v.data(), eo_v.size() * sizeof(double), s)) ||
