@@ -1011,6 +1011,11 @@ static qsg_status run_grid_solve(qsg_ctx* ctx, int mode, const qsg_generator* G,
   // ~4 slices (128 rows) per CTA: small systems are latency-bound and gain from spreading out
   // (Kerr N=200: 60 -> 30 us per attempt from 20 to 148 CTAs, profiles/r01_summary.md)
   int grid = static_cast<int>(std::min<long long>(max_grid, std::max<long long>(1, (nblk + 3) / 4)));
+  // ... but mid-size operators (up to 2,560 slices) run best on 128 CTAs, under one per SM: Kerr
+  // mesolve us per attempt at 128 / 176-296 CTAs: N = 150 22.3 / 23.2, N = 200 23.1 / 24.1,
+  // N = 250 24.6 / 25.2, while N = 300 (2,813 slices) wants all 296 (27.3 vs 33.2)
+  // (scripts/probe_cl_env.py QSG_GRID=..., profiles/r02_small_grid.log)
+  if (nblk < 2560) grid = std::min(grid, 128);
   if (const char* eg = std::getenv("QSG_GRID")) grid = std::max(1, std::min(max_grid, std::atoi(eg)));
   grid = static_cast<int>(std::min<long long>(grid, nblk));
   // Small systems (scripts/probe_small_grid.py, profiles/r02_small_grid.log, Kerr mesolve us per
