@@ -961,7 +961,13 @@ __global__ void __launch_bounds__(kThreads, QSG_GRID_MINB) dp5_grid_kernel(const
 // barrier's L1 invalidation matters. Control, events and the PI controller are the grid engine's
 // (Ctl, begin_attempt, finish_attempt), replicated identically in every CTA; reductions are CTA
 // partials read by every CTA from every CTA's shared memory in rank order (deterministic).
-constexpr int kClThreads = 512;
+// 12 warps per CTA: Kerr N = 20/35/50/70/100 9.70/9.26/9.33/9.94/14.54 us per attempt, against
+// 9.88/9.35/9.44/10.07/15.44 with 16 warps (256 threads: faster to N = 50, 13.2/17.2 at N = 70/100;
+// profiles/r02_cl_kv.log)
+#ifndef QSG_CL_THREADS
+#define QSG_CL_THREADS 384
+#endif
+constexpr int kClThreads = QSG_CL_THREADS;
 constexpr int kEvSmem = 1024;  // events staged in shared memory when the solve has at most this many
 
 __device__ __forceinline__ unsigned cl_rank() {
